@@ -1,0 +1,189 @@
+"""CSR inputs, delta/value symbol domains and baseline-format sizes.
+
+Mirrors the hot-path helpers of /root/reference/pkg/src/csrdtans/sparse.py:
+``CsrMatrix`` (:54-106), ``coo_to_csr`` (:133-144), ``format_size_bytes``
+(:185-198), ``matrix_deltas`` (:289-299), ``value_patterns`` (:302-309).
+``.mtx`` ingestion and the graph-entropy experiment are out of scope (SURVEY
+§2 row 4b).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from .errors import ParameterError
+
+
+@dataclass
+class CooMatrix:
+    rows: int
+    cols: int
+    row_idx: np.ndarray
+    col_idx: np.ndarray
+    values: np.ndarray
+
+    @property
+    def nnz(self) -> int:
+        return len(self.values)
+
+    def validate(self) -> None:
+        if not (len(self.row_idx) == len(self.col_idx) == len(self.values)):
+            raise ParameterError("COO arrays must have equal length")
+        if self.nnz and (
+            self.row_idx.min() < 0 or self.row_idx.max() >= self.rows
+            or self.col_idx.min() < 0 or self.col_idx.max() >= self.cols
+        ):
+            raise ParameterError("COO index out of range")
+
+
+@dataclass
+class CsrMatrix:
+    rows: int
+    cols: int
+    row_start: np.ndarray
+    col_idx: np.ndarray
+    values: np.ndarray
+
+    @property
+    def nnz(self) -> int:
+        return len(self.values)
+
+    @property
+    def value_width(self) -> int:
+        return self.values.dtype.itemsize
+
+    def row_cols(self, i: int) -> np.ndarray:
+        return self.col_idx[self.row_start[i]: self.row_start[i + 1]]
+
+    def row_values(self, i: int) -> np.ndarray:
+        return self.values[self.row_start[i]: self.row_start[i + 1]]
+
+    def validate(self) -> None:
+        """sparse.py:76-91 — shape, span, monotone rows, ascending columns."""
+        if len(self.row_start) != self.rows + 1:
+            raise ParameterError("row_start must have rows + 1 entries")
+        if self.row_start[0] != 0 or self.row_start[-1] != self.nnz:
+            raise ParameterError("row_start must span [0, nnz]")
+        if np.any(np.diff(self.row_start) < 0):
+            raise ParameterError("row_start must be nondecreasing")
+        if self.nnz:
+            if self.col_idx.min() < 0 or self.col_idx.max() >= self.cols:
+                raise ParameterError("column index out of range")
+            deltas = np.diff(self.col_idx)
+            starts = self.row_start[1:-1]
+            inner = np.ones(self.nnz - 1, dtype=bool)
+            inner[starts[(starts > 0) & (starts < self.nnz)] - 1] = False
+            if np.any(deltas[inner] <= 0):
+                raise ParameterError("columns must be strictly ascending per row")
+
+    def __eq__(self, other) -> bool:
+        """Bitwise equality of structure and value bit patterns (sparse.py:93-106)."""
+        if not isinstance(other, CsrMatrix):
+            return NotImplemented
+        return (
+            self.rows == other.rows
+            and self.cols == other.cols
+            and np.array_equal(self.row_start, other.row_start)
+            and np.array_equal(self.col_idx, other.col_idx)
+            and self.values.dtype == other.values.dtype
+            and np.array_equal(
+                self.values.view(np.uint64 if self.value_width == 8 else np.uint32),
+                other.values.view(np.uint64 if self.value_width == 8 else np.uint32),
+            )
+        )
+
+
+def coo_to_csr(m: CooMatrix) -> CsrMatrix:
+    """Sort by (row, col) and compress; duplicates rejected (sparse.py:133-144)."""
+    m.validate()
+    order = np.lexsort((m.col_idx, m.row_idx))
+    r = np.asarray(m.row_idx)[order]
+    c = np.asarray(m.col_idx)[order]
+    v = np.asarray(m.values)[order]
+    if len(r) > 1 and np.any((np.diff(r) == 0) & (np.diff(c) == 0)):
+        raise ParameterError("duplicate (row, col) entry")
+    row_start = np.zeros(m.rows + 1, dtype=np.int64)
+    np.cumsum(np.bincount(r, minlength=m.rows), out=row_start[1:])
+    return CsrMatrix(m.rows, m.cols, row_start, c.astype(np.int64), v)
+
+
+def sell_widths(m: CsrMatrix, slice_height: int = 32) -> np.ndarray:
+    """Per-slice max row length (sparse.py:147-155), vectorised."""
+    nnz_row = np.diff(np.asarray(m.row_start, dtype=np.int64))
+    nslices = max(1, -(-m.rows // slice_height)) if m.rows else 1
+    padded = np.zeros(nslices * slice_height, dtype=np.int64)
+    padded[: m.rows] = nnz_row
+    return padded.reshape(nslices, slice_height).max(axis=1)
+
+
+def format_size_bytes(m: CsrMatrix, fmt: str, value_width: int) -> int:
+    """Byte size in a baseline format with 4-byte indices (sparse.py:185-198).
+
+    The denominator of the compression ratio: min over coo/csr/sell.
+    """
+    if value_width not in (4, 8):
+        raise ParameterError("value_width must be 4 or 8 bytes")
+    fmt = fmt.lower()
+    if fmt == "coo":
+        return m.nnz * (4 + 4 + value_width)
+    if fmt == "csr":
+        return m.nnz * (4 + value_width) + 4 * (m.rows + 1)
+    if fmt == "sell":
+        widths = sell_widths(m, 32)
+        return int(widths.sum()) * 32 * (4 + value_width) + 4 * (len(widths) + 1)
+    raise ParameterError(f"unknown format {fmt!r}")
+
+
+def matrix_deltas(m: CsrMatrix) -> np.ndarray:
+    """Per-row delta encoding of column indices (sparse.py:289-299)."""
+    if m.nnz == 0:
+        return np.zeros(0, dtype=np.int64)
+    col = np.asarray(m.col_idx, dtype=np.int64)
+    d = np.empty(m.nnz, dtype=np.int64)
+    d[0] = col[0]
+    d[1:] = np.diff(col)
+    starts = np.asarray(m.row_start[:-1], dtype=np.int64)
+    starts = starts[starts < m.nnz]
+    d[starts] = col[starts]
+    return d
+
+
+def value_patterns(values: np.ndarray) -> np.ndarray:
+    """Raw bit patterns of the value array (sparse.py:302-309)."""
+    width = values.dtype.itemsize
+    if width == 8:
+        return np.ascontiguousarray(values).view(np.uint64)
+    if width == 4:
+        return np.ascontiguousarray(values).view(np.uint32)
+    raise ParameterError(f"unsupported value width {width}")
+
+
+def reference_spmv(m: CsrMatrix, x: np.ndarray, y: np.ndarray) -> np.ndarray:
+    """The reference's CSR SpMV utility (sparse.py:330-353), numpy on host.
+
+    Part of the mirrored public API (a plain CSR product used for checking
+    and for the compression-free comparison); the dtANS ``spmv`` never calls
+    it.  Per row: acc = +0.0; acc = fl(acc + fl(v * x[c])) left to right;
+    result fl(acc + y).
+    """
+    x = np.asarray(x)
+    y = np.asarray(y)
+    if len(x) != m.cols or len(y) != m.rows:
+        raise ParameterError("dimension mismatch")
+    dtype = m.values.dtype
+    x = x.astype(dtype, copy=False)
+    y = y.astype(dtype, copy=False)
+    acc = np.zeros(m.rows, dtype=dtype)
+    nnz_row = np.diff(m.row_start)
+    if m.nnz:
+        order = np.argsort(-nnz_row, kind="stable")
+        base = m.row_start[:-1][order]
+        maxn = int(nnz_row.max())
+        active = np.searchsorted(-nnz_row[order], -np.arange(1, maxn + 1), side="right")
+        for q in range(maxn):
+            a = int(active[q])
+            idx = base[:a] + q
+            acc[order[:a]] += m.values[idx] * x[m.col_idx[idx]]
+    return acc + y

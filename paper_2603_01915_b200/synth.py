@@ -1,0 +1,132 @@
+"""Synthetic matrices of the five BASELINE.json configurations.
+
+All generators are seeded and vectorised (numpy), and return a
+``CsrMatrix`` with strictly ascending columns per row.  There is no network
+in this environment, so these shapes stand in for SuiteSparse inputs.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from .sparse import CsrMatrix
+
+
+def fig1() -> CsrMatrix:
+    """The 4x4 running example (reference tests/test_sparse.py:27-39)."""
+    row_start = np.array([0, 2, 4, 5, 6], dtype=np.int64)
+    cols = np.array([1, 3, 0, 2, 1, 3], dtype=np.int64)
+    vals = np.array([7.0, 5.0, 3.0, 2.0, 4.0, 1.0])
+    return CsrMatrix(4, 4, row_start, cols, vals)
+
+
+def _csr_from_sorted_codes(rows: int, cols: int, r: np.ndarray, c: np.ndarray,
+                           v: np.ndarray) -> CsrMatrix:
+    row_start = np.zeros(rows + 1, dtype=np.int64)
+    np.cumsum(np.bincount(r, minlength=rows), out=row_start[1:])
+    return CsrMatrix(rows, cols, row_start, c.astype(np.int64), v)
+
+
+def config1_random(n: int = 4096, nnz: int = 2**15, seed: int = 0) -> CsrMatrix:
+    """Config 1: uniform random pattern, N(0,1) fp64 values."""
+    rng = np.random.default_rng(seed)
+    flat = rng.choice(n * n, nnz, replace=False)
+    r, c = np.divmod(flat, n)
+    v = rng.standard_normal(nnz)
+    order = np.lexsort((c, r))
+    return _csr_from_sorted_codes(n, n, r[order], c[order], v[order])
+
+
+def laplacian_2d(g: int, dtype=np.float64) -> CsrMatrix:
+    """Config 2: 5-point Laplacian on a g x g grid (diag 4, neighbours -1)."""
+    n = g * g
+    i = np.arange(n, dtype=np.int64)
+    a, b = np.divmod(i, g)
+    offs = np.array([-g, -1, 0, 1, g], dtype=np.int64)
+    valid = np.stack([a > 0, b > 0, np.ones(n, bool), b < g - 1, a < g - 1], axis=1)
+    cols = i[:, None] + offs[None, :]
+    vals = np.where(offs == 0, 4.0, -1.0).astype(dtype)
+    vals = np.broadcast_to(vals, (n, 5))
+    row_start = np.zeros(n + 1, dtype=np.int64)
+    np.cumsum(valid.sum(axis=1), out=row_start[1:])
+    return CsrMatrix(n, n, row_start, cols[valid], np.ascontiguousarray(vals[valid]))
+
+
+def banded(rows: int, band: int = 27, levels: int = 256, seed: int = 0,
+           positive: bool = False, dtype=np.float64) -> CsrMatrix:
+    """Configs 4/5: FEM-like band of ``band`` entries centred on the
+    diagonal (clipped at the edges), values i.i.d. from a ``levels``-level
+    alphabet (linspace(-1,1) or, for power iteration, (1..levels)/levels)."""
+    half = band // 2
+    i = np.arange(rows, dtype=np.int64)
+    lo = np.maximum(0, i - half)
+    hi = np.minimum(rows, i - half + band)
+    cnt = hi - lo
+    row_start = np.zeros(rows + 1, dtype=np.int64)
+    np.cumsum(cnt, out=row_start[1:])
+    nnz = int(row_start[-1])
+    row_of = np.repeat(i, cnt)
+    cols = lo[row_of] + (np.arange(nnz, dtype=np.int64) - row_start[row_of])
+    if positive:
+        alphabet = (np.arange(levels, dtype=np.float64) + 1.0) / levels
+    else:
+        alphabet = np.linspace(-1.0, 1.0, levels)
+    rng = np.random.default_rng(seed)
+    vals = alphabet.astype(dtype)[rng.integers(0, levels, nnz)]
+    return CsrMatrix(rows, rows, row_start, cols, vals)
+
+
+def rmat(scale: int, nnz: int, seed: int = 0, probs=(57, 19, 19, 5),
+         dtype=np.float32, batch: int = 1 << 24) -> CsrMatrix:
+    """Config 3: R-MAT (a,b,c,d)=(.57,.19,.19,.05) adjacency, edges drawn
+    until ``nnz`` unique (first occurrences in draw order kept), values 1.0.
+    Quadrant choice uses integer percent draws so it is exact."""
+    a, b, c, _ = probs
+    n = 1 << scale
+    rng = np.random.default_rng(seed)
+    seen = np.zeros(0, dtype=np.int64)
+    while len(seen) < nnz:
+        need = int((nnz - len(seen)) * 1.15) + 1024
+        m = min(batch, need)
+        r = np.zeros(m, dtype=np.int64)
+        cc = np.zeros(m, dtype=np.int64)
+        for _ in range(scale):
+            u = rng.integers(0, 100, m, dtype=np.uint8)
+            rbit = u >= a + b
+            cbit = ((u >= a) & (u < a + b)) | (u >= a + b + c)
+            r = (r << 1) | rbit
+            cc = (cc << 1) | cbit
+        codes = (r << scale) | cc
+        allc = np.concatenate([seen, codes])
+        _, first = np.unique(allc, return_index=True)
+        first.sort()
+        seen = allc[first]
+    seen = np.sort(seen[:nnz])
+    r, cc = np.divmod(seen, n)
+    return _csr_from_sorted_codes(n, n, r, cc, np.ones(nnz, dtype=dtype))
+
+
+def vectors(m: CsrMatrix, seed_x: int = 1, seed_y: int = 2, y_zero=False):
+    """x ~ N(0,1) (seed 1), y ~ N(0,1) (seed 2) in the matrix precision."""
+    dtype = m.values.dtype
+    x = np.random.default_rng(seed_x).standard_normal(m.cols).astype(dtype)
+    if y_zero:
+        y = np.zeros(m.rows, dtype=dtype)
+    else:
+        y = np.random.default_rng(seed_y).standard_normal(m.rows).astype(dtype)
+    return x, y
+
+
+def config(name: str) -> CsrMatrix:
+    """Full-size matrices of BASELINE.json configs by short name."""
+    if name == "config1":
+        return config1_random()
+    if name == "laplacian":
+        return laplacian_2d(2591)
+    if name == "rmat":
+        return rmat(23, 2**27)
+    if name == "banded27":
+        return banded(-(-2**28 // 27), 27)
+    if name == "banded32":
+        return banded(2**24, 32, positive=True)
+    raise KeyError(name)
