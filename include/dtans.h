@@ -1,0 +1,150 @@
+/*
+ * dtans.h — the C ABI of libdtans.so (B200-native CSR-dtANS SpMV).
+ *
+ * The reference (/root/reference/pkg/src/csrdtans) is a pure-Python package
+ * with no FFI; its plugin surface for this path is the Python API
+ *   encode_matrix  container.py:126-204
+ *   spmv           container.py:554-596
+ *   decode_matrix  container.py:524-531
+ *   quantize       entropy.py:223-321
+ * Each entry point below replaces the body of one of those functions; the
+ * Python package paper_2603_01915_b200 binds them with ctypes exactly as a
+ * maintainer of the reference would.
+ *
+ * Plain pointers and sizes only; no torch types.  All functions return a
+ * dtans_status; on failure dtans_last_error() holds a message (per thread).
+ * Device pointers are CUDA global-memory pointers on the handle's device;
+ * "stream" is a cudaStream_t passed as void* (NULL = legacy default stream).
+ */
+#ifndef DTANS_H
+#define DTANS_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    DTANS_OK = 0,
+    DTANS_E_PARAM = 1,    /* -> ParameterError (entropy.py:18)            */
+    DTANS_E_CODING = 2,   /* -> CodingError    (entropy.py:22)            */
+    DTANS_E_CORRUPT = 3,  /* -> CorruptStream  (entropy.py:26)            */
+    DTANS_E_CUDA = 4,     /* CUDA runtime failure                         */
+    DTANS_E_NOMEM = 5,    /* host or device allocation failed             */
+    DTANS_E_NODEVICE = 6  /* no CUDA device: the product has no CPU path  */
+} dtans_status;
+
+/* Message for the last failure on the calling thread ("" if none). */
+const char *dtans_last_error(void);
+
+/* ABI version (bumped when a struct layout changes). */
+int dtans_abi_version(void);
+
+/* ------------------------------------------------------------------ */
+/* Encoder (host, C++17, multithreaded).  Byte-identical to the
+ * reference encode_matrix (container.py:126-204). */
+
+typedef struct {
+    int64_t rows, cols, nnz;
+    const int64_t *row_start; /* rows + 1 */
+    const int64_t *col_idx;   /* nnz, strictly ascending per row */
+    const void *values;       /* nnz values already in the container precision */
+    int32_t precision;        /* 4 (f32) or 8 (f64) */
+} dtans_csr_view;
+
+typedef struct {
+    int32_t k_log2;              /* 12 (K = 4096)                           */
+    int32_t m_log2;              /* <= 8 (M <= 256)                         */
+    const uint32_t *perm_delta;  /* K-entry slot permutation or NULL       */
+    const uint32_t *perm_value;  /* (numpy default_rng(seed).permutation)  */
+    int32_t threads;             /* 0 = all hardware threads               */
+} dtans_encode_opts;
+
+/* Encoder output, allocated by the library; release with
+ * dtans_encoded_free.  tables holds K serialized slot records in the
+ * reference layout (container.py:604-609): 16 B (f64) / 12 B (f32). */
+typedef struct {
+    int64_t rows, cols, nnz, nslices, nwords;
+    int32_t precision, rec_size;
+    uint8_t *tables;       /* K * rec_size bytes */
+    uint32_t *row_symbols; /* rows              */
+    uint64_t *directory;   /* nslices + 1       */
+    uint32_t *stream;      /* nwords            */
+} dtans_encoded;
+
+/* Replaces encode_matrix (container.py:126-204): validation (sparse.py:76-91),
+ * distributions (container.py:112-114), quantize (entropy.py:223-321) x2,
+ * build_tables (entropy.py:404-436) x2, per-row dtans_encode
+ * (codec.py:296-368), interleave_warp (container.py:283-317). */
+int dtans_encode(const dtans_csr_view *m, const dtans_encode_opts *opts,
+                 dtans_encoded *out);
+void dtans_encoded_free(dtans_encoded *e);
+
+/* Replaces quantize (entropy.py:223-321) for one domain.  symbols ascending,
+ * counts >= 1.  Writes mult[n] (0 = escaped), *esc_mult, *esc_slots.
+ * never_retain: n_never symbols that are always escaped. */
+int dtans_quantize(int64_t n, const uint64_t *symbols, const int64_t *counts,
+                   int32_t k, int32_t m, int32_t raw_width_bits,
+                   int64_t n_never, const uint64_t *never_retain,
+                   int32_t *mult, int32_t *esc_mult, int32_t *esc_slots);
+
+/* ------------------------------------------------------------------ */
+/* Device container (sm_100a). */
+
+typedef struct dtans_dev dtans_dev; /* opaque */
+
+/* A container in host memory, fields as in CsrDtansContainer
+ * (container.py:57-70) with the tables as the serialized record block. */
+typedef struct {
+    int64_t rows, cols, nnz, nslices, nwords;
+    int32_t precision;
+    const uint8_t *tables;       /* K * (16 | 12) bytes */
+    const uint32_t *row_symbols; /* rows */
+    const uint64_t *directory;   /* nslices + 1 */
+    const uint32_t *stream;      /* nwords */
+} dtans_container_view;
+
+/* Upload + re-layout for the kernel (split per-domain slot tables, a
+ * 16-byte padded stream, per-tile plans).  Synchronous. */
+int dtans_upload(const dtans_container_view *c, int device, dtans_dev **out);
+void dtans_free(dtans_dev *h);
+
+/* Device-memory footprint of the handle, and the launch plan it chose. */
+int dtans_info(const dtans_dev *h, int64_t *device_bytes, int32_t *ctas,
+               int32_t *warps_per_cta, int32_t *smem_bytes);
+
+/* y' = A x + y on device pointers (x: cols, y/out: rows, container
+ * precision).  y may be NULL (y' = A x: the power-iteration form).
+ * out may alias y.  Replaces spmv (container.py:554-596) body:
+ * _decode_slice_range (:370-521) fused with _accumulate_rows (:534-551).
+ * Asynchronous on `stream`; errors in the stream surface in dtans_check. */
+int dtans_spmv_f64(dtans_dev *h, const double *x, const double *y, double *out,
+                   void *stream);
+int dtans_spmv_f32(dtans_dev *h, const float *x, const float *y, float *out,
+                   void *stream);
+
+/* Same product with HOST x, y, out (pageable or pinned): H2D copy, kernel,
+ * D2H copy, synchronize, consumption check.  The end-to-end entry point a
+ * ctypes binding of spmv(c, x, y) calls. */
+int dtans_spmv_host(dtans_dev *h, const void *x, const void *y, void *out);
+
+/* Bit-exact decode on device: row_start (device, rows+1, int64) must be
+ * the prefix sum of row_symbols/2; writes cols (int64) and value bit
+ * patterns (u64 for f64, u32 for f32).  Replaces decode_matrix
+ * (container.py:524-531). */
+int dtans_decode(dtans_dev *h, const int64_t *row_start, int64_t *cols,
+                 void *valbits, void *stream);
+
+/* Synchronize `stream` and read + clear the device error word set by the
+ * kernels (consumption mismatch / out-of-range column) -> DTANS_E_CORRUPT. */
+int dtans_check(dtans_dev *h, void *stream);
+
+/* Number of dtANS kernels launched by this handle so far (bench evidence). */
+int64_t dtans_launch_count(const dtans_dev *h);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DTANS_H */

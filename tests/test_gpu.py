@@ -1,0 +1,88 @@
+"""GPU parity tests: the sm_100a kernels against the reference goldens and
+the oracle.  Run on a B200 with `pytest -m gpu`."""
+
+import numpy as np
+import pytest
+
+import golden_cases as G
+import paper_2603_01915_b200 as P
+from paper_2603_01915_b200 import synth
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover - CPU container
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+SPMV_CASES = [n for n in G.names() if "spmv" in G.load(n)]
+
+
+@pytest.mark.parametrize("name", SPMV_CASES)
+def test_spmv_bitwise_reference(name):
+    rec = G.load(name)
+    c = P.encode_matrix(G.matrix(rec), **G.encode_kwargs(rec))
+    out = P.spmv(c, rec["x"], rec["y"])
+    assert G.same_bits_or_nan(out, rec["spmv"])
+
+
+@pytest.mark.parametrize("name", G.names())
+def test_decode_bit_exact(name):
+    rec = G.load(name)
+    m = G.matrix(rec)
+    c = P.encode_matrix(m, **G.encode_kwargs(rec))
+    d = P.decode_matrix(c)
+    vdt = np.float64 if c.precision == 8 else np.float32
+    assert d == P.CsrMatrix(m.rows, m.cols, m.row_start, m.col_idx, m.values.astype(vdt))
+
+
+@pytest.mark.parametrize("name", [n for n in SPMV_CASES if "container" in G.load(n)])
+def test_spmv_from_reference_bytes(name):
+    rec = G.load(name)
+    c = P.deserialize(rec["container"].tobytes())
+    out = P.spmv(c, rec["x"], rec["y"])
+    assert G.same_bits_or_nan(out, rec["spmv"])
+
+
+def test_corrupt_directory_raises():
+    rec = G.load("laplacian_g48")
+    c = P.deserialize(rec["container"].tobytes())
+    d = c.directory.copy()
+    d[1:-1] += 1  # every slice boundary shifted by one word
+    c.directory = d
+    with pytest.raises(P.CorruptStream):
+        P.spmv(c, rec["x"], rec["y"])
+
+
+def test_device_tensor_path_and_y_none():
+    m = synth.laplacian_2d(300)
+    x, y = synth.vectors(m)
+    c = P.encode_matrix(m)
+    dev = c.device(0)
+    xt = torch.from_numpy(x).cuda()
+    yt = torch.from_numpy(y).cuda()
+    out = dev.spmv(xt, yt)
+    dev.check()
+    oc = O.parse(P.serialize(c))
+    assert G.same_bits_or_nan(out.cpu().numpy(), O.spmv(oc, x, y))
+    out0 = dev.spmv(xt, None)
+    dev.check()
+    assert G.same_bits_or_nan(out0.cpu().numpy(), O.spmv(oc, x, np.zeros_like(y)))
+
+
+@pytest.mark.parametrize("gen", [
+    lambda: synth.laplacian_2d(700),
+    lambda: synth.banded(60000, 27),
+    lambda: synth.banded(40000, 32, positive=True),
+    lambda: synth.rmat(14, 200000),
+    lambda: synth.rmat(12, 40000, dtype=np.float64),
+    lambda: synth.config1_random(20000, 300000, seed=4),
+])
+def test_larger_matrices_vs_oracle(gen):
+    m = gen()
+    x, y = synth.vectors(m)
+    c = P.encode_matrix(m)
+    assert P.decode_matrix(c) == m
+    out = P.spmv(c, x, y)
+    ref = O.spmv(O.parse(P.serialize(c)), x, y, threads=8)
+    assert G.same_bits_or_nan(out, ref)
