@@ -4,6 +4,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -18,8 +19,7 @@ struct dtans_dev {
     int32_t precision = 8;
     void *d_base = nullptr;     // single allocation for all container arrays
     size_t d_bytes = 0;
-    uint2 *d_dtab = nullptr;
-    void *d_vtab = nullptr;
+    uint32_t *d_tables = nullptr;
     uint32_t *d_row_symbols = nullptr;
     uint64_t *d_directory = nullptr;
     uint32_t *d_stream = nullptr;
@@ -27,8 +27,10 @@ struct dtans_dev {
     // staging buffers for the host-pointer entry point
     void *d_io = nullptr;
     size_t io_bytes = 0;
-    int ctas = 0, threads = 512, smem = 0;
+    dev::KernelArgs base{};     // launch-invariant kernel arguments
+    int ctas = 0, threads = 1024, smem = 0;
     int64_t launches = 0;
+    int64_t staged_slices = 0;  // slices whose stream fits a ring buffer
 };
 
 namespace {
@@ -46,35 +48,112 @@ int cuda_fail(cudaError_t e, const char *what)
 
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
-template <typename V>
-int configure(dtans_dev *h)
+// Compact slot tables: entry = digit | (base-1) << 8 | id << 16 with id the
+// index of the slot's symbol in the domain dictionary (ascending retained
+// symbols) and id = n_retained for escape slots.
+struct TableBlock {
+    std::vector<uint32_t> words;  // [dtab][vtab][ddict (+pad)][vdict (+pad)]
+    int32_t off_ddict = 0, off_vdict = 0;
+    uint32_t nd = 0, nv = 0;
+};
+
+TableBlock build_table_block(const uint8_t *recs, int precision)
 {
-    using Entry = typename dev::ValueTraits<V>::Entry;
-    h->smem = (int)(dev::kSlots * (sizeof(uint2) + sizeof(Entry)));
-    CK(cudaFuncSetAttribute(dev::dtans_spmv_kernel<V>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            h->smem),
-       "cudaFuncSetAttribute");
-    int per_sm = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dev::dtans_spmv_kernel<V>, h->threads,
-                                                     h->smem),
-       "occupancy");
-    if (per_sm < 1) return fail(DTANS_E_CUDA, "kernel does not fit on an SM");
-    int sms = 0;
-    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device), "sm count");
-    const int64_t warps_needed = h->nslices;
-    const int64_t ctas_needed = (warps_needed + h->threads / 32 - 1) / (h->threads / 32);
-    h->ctas = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)sms * per_sm, ctas_needed));
-    return DTANS_OK;
+    const int rec = precision == 8 ? 16 : 12;
+    const uint64_t vsent = precision == 8 ? ~0ull : 0xFFFFFFFFull;
+    std::vector<uint64_t> dsym(kK), vsym(kK);
+    std::vector<uint8_t> desc(kK), vesc(kK), ddig(kK), dbm1(kK), vdig(kK), vbm1(kK);
+    for (int j = 0; j < kK; j++) {
+        const uint8_t *r = recs + (size_t)j * rec;
+        uint64_t vs = 0;
+        uint32_t ds = 0;
+        if (precision == 8) {
+            memcpy(&vs, r, 8);
+            memcpy(&ds, r + 8, 4);
+            r += 12;
+        } else {
+            uint32_t v32;
+            memcpy(&v32, r, 4);
+            vs = v32;
+            memcpy(&ds, r + 4, 4);
+            r += 8;
+        }
+        dsym[j] = ds;
+        vsym[j] = vs;
+        desc[j] = ds == (uint32_t)kDeltaSentinel;
+        vesc[j] = vs == vsent;
+        ddig[j] = r[0];
+        dbm1[j] = r[1];
+        vdig[j] = r[2];
+        vbm1[j] = r[3];
+    }
+    auto dict = [](const std::vector<uint64_t> &sym, const std::vector<uint8_t> &esc) {
+        std::vector<uint64_t> u;
+        for (int j = 0; j < kK; j++)
+            if (!esc[j]) u.push_back(sym[j]);
+        std::sort(u.begin(), u.end());
+        u.erase(std::unique(u.begin(), u.end()), u.end());
+        return u;
+    };
+    const std::vector<uint64_t> dd = dict(dsym, desc), vd = dict(vsym, vesc);
+    TableBlock tb;
+    tb.nd = (uint32_t)dd.size();
+    tb.nv = (uint32_t)vd.size();
+    const size_t dict_d_words = align_up(dd.size() + 1, 4);
+    const size_t vw = precision == 8 ? 2 : 1;
+    const size_t dict_v_words = align_up((vd.size() + 1) * vw, 4);
+    tb.words.assign(2 * kK + dict_d_words + dict_v_words, 0);
+    tb.off_ddict = (int32_t)(2 * kK * 4);
+    tb.off_vdict = (int32_t)((2 * kK + dict_d_words) * 4);
+    for (int j = 0; j < kK; j++) {
+        // id field = byte offset of the symbol in its dictionary; escapes
+        // point at the dummy slot after the retained symbols
+        const uint32_t did = 4u * (desc[j] ? tb.nd
+                                           : (uint32_t)(std::lower_bound(dd.begin(), dd.end(), dsym[j]) - dd.begin()));
+        const uint32_t vid = (uint32_t)(4 * vw) *
+                             (vesc[j] ? tb.nv
+                                      : (uint32_t)(std::lower_bound(vd.begin(), vd.end(), vsym[j]) - vd.begin()));
+        tb.words[j] = (uint32_t)ddig[j] | ((uint32_t)dbm1[j] << 8) | (did << 16);
+        tb.words[kK + j] = (uint32_t)vdig[j] | ((uint32_t)vbm1[j] << 8) | (vid << 16);
+    }
+    for (size_t i = 0; i < dd.size(); i++) tb.words[2 * kK + i] = (uint32_t)dd[i];
+    uint32_t *vdw = tb.words.data() + 2 * kK + dict_d_words;
+    for (size_t i = 0; i < vd.size(); i++) {
+        if (vw == 2) {
+            vdw[2 * i] = (uint32_t)vd[i];
+            vdw[2 * i + 1] = (uint32_t)(vd[i] >> 32);
+        } else {
+            vdw[i] = (uint32_t)vd[i];
+        }
+    }
+    return tb;
+}
+
+// Dispatch on the compile-time CTA size.
+template <typename V, class F>
+int with_kernel(int threads, F &&f)
+{
+    switch (threads) {
+    case 768:
+        return f(dev::dtans_kernel<V, false, true, 768>, dev::dtans_kernel<V, false, false, 768>,
+                 dev::dtans_kernel<V, true, false, 768>);
+    default:
+        return f(dev::dtans_kernel<V, false, true, 1024>, dev::dtans_kernel<V, false, false, 1024>,
+                 dev::dtans_kernel<V, true, false, 1024>);
+    }
 }
 
 template <typename V>
-int launch(dtans_dev *h, const V *x, const V *y, V *out, const int64_t *row_start, int64_t *cols,
-           void *vals, int decode_only, cudaStream_t st)
+int configure(dtans_dev *h, const TableBlock &tb, const uint64_t *directory)
 {
-    if (h->nslices == 0) return DTANS_OK;
-    dev::KernelArgs a;
-    a.dtab = h->d_dtab;
-    a.vtab = h->d_vtab;
+    dev::KernelArgs &a = h->base;
+    a.tables = h->d_tables;
+    a.table_bytes = (int32_t)(tb.words.size() * 4);
+    a.off_ddict = tb.off_ddict;
+    a.off_vdict = tb.off_vdict;
+    a.desc_min = (4u * tb.nd) << 16;
+    a.vesc_min = ((uint32_t)(sizeof(V)) * tb.nv) << 16;
+    a.pads_ok = tb.nd > 0 && tb.nv > 0;
     a.row_symbols = h->d_row_symbols;
     a.directory = h->d_directory;
     a.stream = h->d_stream;
@@ -82,15 +161,76 @@ int launch(dtans_dev *h, const V *x, const V *y, V *out, const int64_t *row_star
     a.cols = h->cols;
     a.nslices = h->nslices;
     a.nwords = h->nwords;
+    a.err = h->d_err;
+    int max_optin = 0, sms = 0;
+    CK(cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->device), "attr");
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device), "sm count");
+    size_t off = (size_t)a.table_bytes;
+    off = align_up(off, 16);
+    a.off_bars = (int32_t)off;
+    off += dev::kMaxWarps * dev::kRing * 8;
+    off = align_up(off, 16);
+    a.off_meta = (int32_t)off;
+    off += dev::kMaxWarps * dev::kRing * sizeof(dev::SliceMeta);
+    off = align_up(off, 128);
+    a.off_bufs = (int32_t)off;
+    // ring buffer size: the largest 16-byte-aligned slice window, capped by
+    // what fits; bigger slices are decoded straight from global memory.
+    uint64_t max_words = 4;
+    for (int64_t s = 0; s < h->nslices; s++) {
+        const uint64_t lo = directory[s] & ~3ull, hi = (directory[s + 1] + 3) & ~3ull;
+        max_words = std::max<uint64_t>(max_words, hi - lo);
+    }
+    const char *env_t = getenv("DTANS_THREADS");
+    h->threads = env_t ? atoi(env_t) : 1024;
+    if (h->threads != 1024 && h->threads != 768) h->threads = 1024;
+    const int warps = h->threads / 32;
+    const int64_t budget =
+        ((int64_t)max_optin - (int64_t)off - dev::kOverrunWords * 4) / (warps * dev::kRing * 4);
+    if (budget < 4) return fail(DTANS_E_CUDA, "coding tables leave no shared memory for staging");
+    a.bufw = (int32_t)std::min<int64_t>((int64_t)align_up(max_words, 4), budget / 4 * 4);
+    h->staged_slices = 0;
+    for (int64_t s = 0; s < h->nslices; s++) {
+        const uint64_t lo = directory[s] & ~3ull, hi = (directory[s + 1] + 3) & ~3ull;
+        if (hi - lo <= (uint64_t)a.bufw) h->staged_slices++;
+    }
+    h->smem = (int)(off + ((size_t)warps * dev::kRing * a.bufw + dev::kOverrunWords) * 4);
+    int per_sm = 0;
+    int rc = with_kernel<V>(h->threads, [&](auto kspmv, auto kspmv0, auto kdec) -> int {
+        CK(cudaFuncSetAttribute(kspmv, cudaFuncAttributeMaxDynamicSharedMemorySize, h->smem), "cudaFuncSetAttribute");
+        CK(cudaFuncSetAttribute(kspmv0, cudaFuncAttributeMaxDynamicSharedMemorySize, h->smem), "cudaFuncSetAttribute");
+        CK(cudaFuncSetAttribute(kdec, cudaFuncAttributeMaxDynamicSharedMemorySize, h->smem), "cudaFuncSetAttribute");
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kspmv, h->threads, h->smem), "occupancy");
+        return DTANS_OK;
+    });
+    if (rc) return rc;
+    if (per_sm < 1) return fail(DTANS_E_CUDA, "kernel does not fit on an SM");
+    const int64_t ctas_needed = (h->nslices + warps - 1) / warps;
+    h->ctas = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)sms * per_sm, ctas_needed));
+    return DTANS_OK;
+}
+
+template <typename V>
+int launch(dtans_dev *h, const V *x, const V *y, V *out, const int64_t *row_start, int64_t *cols,
+           void *vals, bool decode_only, cudaStream_t st)
+{
+    if (h->nslices == 0) return DTANS_OK;
+    dev::KernelArgs a = h->base;
     a.x = x;
     a.y = y;
     a.out = out;
     a.row_start = row_start;
     a.dec_cols = cols;
     a.dec_vals = vals;
-    a.err = h->d_err;
-    a.decode_only = decode_only;
-    dev::dtans_spmv_kernel<V><<<h->ctas, h->threads, h->smem, st>>>(a);
+    with_kernel<V>(h->threads, [&](auto kspmv, auto kspmv0, auto kdec) -> int {
+        if (decode_only)
+            kdec<<<h->ctas, h->threads, h->smem, st>>>(a);
+        else if (y != nullptr)
+            kspmv<<<h->ctas, h->threads, h->smem, st>>>(a);
+        else
+            kspmv0<<<h->ctas, h->threads, h->smem, st>>>(a);
+        return 0;
+    });
     h->launches++;
     CK(cudaGetLastError(), "kernel launch");
     return DTANS_OK;
@@ -110,6 +250,7 @@ extern "C" int dtans_upload(const dtans_container_view *c, int device, dtans_dev
     }
     if (device < 0 || device >= ndev) return fail(DTANS_E_PARAM, "bad device ordinal %d", device);
     CK(cudaSetDevice(device), "cudaSetDevice");
+    if (c->rows >= ((int64_t)1 << 32)) return fail(DTANS_E_PARAM, "the device path needs rows < 2^32");
     const int64_t nsl = (c->rows + kSlice - 1) / kSlice;
     if (c->nslices != nsl) return fail(DTANS_E_PARAM, "nslices does not match rows");
     if ((int64_t)c->directory[nsl] != c->nwords)
@@ -123,50 +264,14 @@ extern "C" int dtans_upload(const dtans_container_view *c, int device, dtans_dev
     h->nslices = nsl;
     h->nwords = c->nwords;
     h->precision = c->precision;
+    const TableBlock tb = build_table_block(c->tables, c->precision);
 
-    // re-laid-out slot tables (see kernels.cuh for the entry formats)
-    const int rec = c->precision == 8 ? 16 : 12;
-    const size_t vent = c->precision == 8 ? 16 : 8;
-    std::vector<uint2> dt(kK);
-    std::vector<uint32_t> vt(kK * vent / 4, 0);
-    const uint64_t vsent = c->precision == 8 ? ~0ull : 0xFFFFFFFFull;
-    for (int j = 0; j < kK; j++) {
-        const uint8_t *r = c->tables + (size_t)j * rec;
-        uint64_t vs = 0;
-        uint32_t ds = 0;
-        if (c->precision == 8) {
-            memcpy(&vs, r, 8);
-            memcpy(&ds, r + 8, 4);
-            r += 12;
-        } else {
-            uint32_t v32;
-            memcpy(&v32, r, 4);
-            vs = v32;
-            memcpy(&ds, r + 4, 4);
-            r += 8;
-        }
-        const uint32_t desc = ds == (uint32_t)kDeltaSentinel;
-        const uint32_t vesc = vs == vsent;
-        dt[j].x = desc ? 0u : ds;
-        dt[j].y = (uint32_t)r[0] | ((uint32_t)r[1] << 8) | (desc << 16);
-        const uint32_t vmeta = (uint32_t)r[2] | ((uint32_t)r[3] << 8) | (vesc << 16);
-        if (c->precision == 8) {
-            const uint64_t v = vesc ? 0 : vs;
-            vt[4 * j + 0] = (uint32_t)v;
-            vt[4 * j + 1] = (uint32_t)(v >> 32);
-            vt[4 * j + 2] = vmeta;
-        } else {
-            vt[2 * j + 0] = vesc ? 0u : (uint32_t)vs;
-            vt[2 * j + 1] = vmeta;
-        }
-    }
-    // one allocation: [dtab][vtab][row_symbols][directory][stream + pad][err]
+    // one allocation: [tables][row_symbols][directory][stream + pad][err]
     size_t off = 0;
-    const size_t o_dt = off; off = align_up(off + kK * sizeof(uint2), 256);
-    const size_t o_vt = off; off = align_up(off + kK * vent, 256);
+    const size_t o_tb = off; off = align_up(off + tb.words.size() * 4, 256);
     const size_t o_rs = off; off = align_up(off + sizeof(uint32_t) * (size_t)std::max<int64_t>(c->rows, 1), 256);
     const size_t o_di = off; off = align_up(off + sizeof(uint64_t) * (size_t)(nsl + 1), 256);
-    const size_t o_st = off; off = align_up(off + sizeof(uint32_t) * (size_t)c->nwords + 64, 256);
+    const size_t o_st = off; off = align_up(off + sizeof(uint32_t) * ((size_t)c->nwords + dev::kOverrunWords), 256);
     const size_t o_er = off; off = align_up(off + 16, 256);
     cudaError_t e = cudaMalloc(&h->d_base, off);
     if (e != cudaSuccess) {
@@ -175,8 +280,7 @@ extern "C" int dtans_upload(const dtans_container_view *c, int device, dtans_dev
     }
     h->d_bytes = off;
     char *b = (char *)h->d_base;
-    h->d_dtab = (uint2 *)(b + o_dt);
-    h->d_vtab = b + o_vt;
+    h->d_tables = (uint32_t *)(b + o_tb);
     h->d_row_symbols = (uint32_t *)(b + o_rs);
     h->d_directory = (uint64_t *)(b + o_di);
     h->d_stream = (uint32_t *)(b + o_st);
@@ -188,17 +292,17 @@ extern "C" int dtans_upload(const dtans_container_view *c, int device, dtans_dev
             if (ce != cudaSuccess) rc = cuda_fail(ce, "upload");
         }
     };
-    cp(h->d_dtab, dt.data(), kK * sizeof(uint2));
-    cp(h->d_vtab, vt.data(), kK * vent);
+    cp(h->d_tables, tb.words.data(), tb.words.size() * 4);
     cp(h->d_row_symbols, c->row_symbols, sizeof(uint32_t) * (size_t)c->rows);
     cp(h->d_directory, c->directory, sizeof(uint64_t) * (size_t)(nsl + 1));
     cp(h->d_stream, c->stream, sizeof(uint32_t) * (size_t)c->nwords);
     if (rc == DTANS_OK) {
-        cudaError_t ce = cudaMemset(h->d_stream + c->nwords, 0, 64);
+        cudaError_t ce = cudaMemset(h->d_stream + c->nwords, 0, sizeof(uint32_t) * dev::kOverrunWords);
         if (ce == cudaSuccess) ce = cudaMemset(h->d_err, 0, 16);
         if (ce != cudaSuccess) rc = cuda_fail(ce, "memset");
     }
-    if (rc == DTANS_OK) rc = c->precision == 8 ? configure<double>(h) : configure<float>(h);
+    if (rc == DTANS_OK)
+        rc = c->precision == 8 ? configure<double>(h, tb, c->directory) : configure<float>(h, tb, c->directory);
     if (rc != DTANS_OK) {
         cudaFree(h->d_base);
         delete h;
@@ -236,7 +340,7 @@ extern "C" int dtans_spmv_f64(dtans_dev *h, const double *x, const double *y, do
     if (!h) return fail(DTANS_E_PARAM, "null handle");
     if (h->precision != 8) return fail(DTANS_E_PARAM, "container precision is f32");
     CK(cudaSetDevice(h->device), "cudaSetDevice");
-    return launch<double>(h, x, y, out, nullptr, nullptr, nullptr, 0, (cudaStream_t)stream);
+    return launch<double>(h, x, y, out, nullptr, nullptr, nullptr, false, (cudaStream_t)stream);
 }
 
 extern "C" int dtans_spmv_f32(dtans_dev *h, const float *x, const float *y, float *out,
@@ -245,7 +349,7 @@ extern "C" int dtans_spmv_f32(dtans_dev *h, const float *x, const float *y, floa
     if (!h) return fail(DTANS_E_PARAM, "null handle");
     if (h->precision != 4) return fail(DTANS_E_PARAM, "container precision is f64");
     CK(cudaSetDevice(h->device), "cudaSetDevice");
-    return launch<float>(h, x, y, out, nullptr, nullptr, nullptr, 0, (cudaStream_t)stream);
+    return launch<float>(h, x, y, out, nullptr, nullptr, nullptr, false, (cudaStream_t)stream);
 }
 
 extern "C" int dtans_check(dtans_dev *h, void *stream)
@@ -285,10 +389,10 @@ extern "C" int dtans_spmv_host(dtans_dev *h, const void *x, const void *y, void 
     int rc;
     if (h->precision == 8)
         rc = launch<double>(h, (const double *)dx, y ? (const double *)dy : nullptr, (double *)dout,
-                            nullptr, nullptr, nullptr, 0, st);
+                            nullptr, nullptr, nullptr, false, st);
     else
         rc = launch<float>(h, (const float *)dx, y ? (const float *)dy : nullptr, (float *)dout,
-                           nullptr, nullptr, nullptr, 0, st);
+                           nullptr, nullptr, nullptr, false, st);
     if (rc) return rc;
     CK(cudaMemcpyAsync(out, dout, es * (size_t)h->rows, cudaMemcpyDeviceToHost, st), "D2H out");
     return dtans_check(h, st);
@@ -300,8 +404,8 @@ extern "C" int dtans_decode(dtans_dev *h, const int64_t *row_start, int64_t *col
     if (!h) return fail(DTANS_E_PARAM, "null handle");
     CK(cudaSetDevice(h->device), "cudaSetDevice");
     if (h->precision == 8)
-        return launch<double>(h, nullptr, nullptr, nullptr, row_start, cols, valbits, 1,
+        return launch<double>(h, nullptr, nullptr, nullptr, row_start, cols, valbits, true,
                               (cudaStream_t)stream);
-    return launch<float>(h, nullptr, nullptr, nullptr, row_start, cols, valbits, 1,
+    return launch<float>(h, nullptr, nullptr, nullptr, row_start, cols, valbits, true,
                          (cudaStream_t)stream);
 }

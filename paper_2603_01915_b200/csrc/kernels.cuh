@@ -1,20 +1,29 @@
 // Fused dtANS decode + SpMV for sm_100a.
 //
-// One warp decodes one 32-row slice, lane i = row 32s+i, exactly the
-// lockstep the container's word order was interleaved for
+// Mapping.  One warp decodes one 32-row slice, lane i = row 32s+i: exactly
+// the lockstep the container's word order was interleaved for
 // (container.py:211-335).  Per lane the decoder runs the reference's
 // per-segment loop (container.py:370-521, codec.py:384-453):
-//   unpack 3 words -> 8 slots, 8 table lookups (shared memory),
+//   unpack 3 words -> 8 slots, 8 slot-table lookups (shared memory),
 //   escape payload event (warp exclusive scan), 2 mixed-radix checks
-//   (extract from the state or load: ballot + popc), 1 unconditional load.
+//   (extract from the state, or load: ballot + popc), 1 unconditional load.
 // The symbols never leave registers: column deltas are prefix-summed,
-// x[col] is gathered and acc = fl(acc + fl(v * x)) runs left to right per
-// row from +0.0 (container.py:534-551) with __dmul_rn/__dadd_rn, so the
-// result is bitwise the reference's.
+// x[col] is gathered, acc = fl(acc + fl(v * x)) runs left to right per row
+// from +0.0 (container.py:534-551) with __dmul_rn/__dadd_rn, so the result
+// is bitwise the reference's.
 //
-// Mixed-radix state: at every segment start d < r < 2^32 (r is divided by
+// Memory.  Each warp owns a ring of kRing shared-memory buffers; lane 0
+// stages the word range [directory[s], directory[s+1]) of the slice it will
+// decode kRing slices later with one cp.async.bulk (TMA bulk copy, 16-byte
+// aligned window) completing on an mbarrier.  The decoder then reads stream
+// words from shared memory.  Slices larger than a buffer are read straight
+// from global memory (same code, generic pointer).  Slot tables are compact
+// u32 entries {digit:8, base-1:8, id:16} per domain (16 KB each) plus
+// dictionaries of the retained symbols, so a CTA needs ~33 KB of tables.
+//
+// Mixed-radix state.  At every segment start d < r < 2^32 (r is divided by
 // 2^32 whenever it reaches 2^32), so the resting state is two u32.  A group
-// of 4 digits is folded into one product in 32-bit arithmetic using the
+// of 4 digits folds into one product in 32-bit arithmetic with the
 // decremented radix Bm1 = b0 b1 b2 b3 - 1 <= 2^32 - 1 (codec.py:127-137):
 //   d' = d*Bm1 + d + D,  r' = r*Bm1 + r       (64-bit, < 2^64)
 // and the check is r' >= 2^32: extract w = lo32(d'), d = hi32(d'),
@@ -27,52 +36,44 @@ namespace dev {
 
 constexpr int kSliceRows = 32;
 constexpr int kSlots = 4096;
+constexpr int kMaxWarps = 32;  // per CTA (1024 threads); smem layout is sized for this
+constexpr int kRing = 3;
 
-// Slot-table entry layouts in shared memory (built by dtans_upload):
-//   delta       : uint2 {sym32, meta}
-//   value (f64) : uint4 {sym_lo, sym_hi, meta, 0}
-//   value (f32) : uint2 {sym32, meta}
-// meta = digit | (base-1) << 8 | escape << 16.
 template <typename V> struct ValueTraits;
 template <> struct ValueTraits<double> {
-    using Entry = uint4;
     using Bits = unsigned long long;
     static constexpr int kPayloadWords = 2;
-    __device__ static inline Bits sym(const uint4 &e)
-    {
-        return ((Bits)e.y << 32) | e.x;
-    }
-    __device__ static inline uint32_t meta(const uint4 &e) { return e.z; }
     __device__ static inline double from_bits(Bits b) { return __longlong_as_double((long long)b); }
     __device__ static inline double mul(double a, double b) { return __dmul_rn(a, b); }
     __device__ static inline double add(double a, double b) { return __dadd_rn(a, b); }
 };
 template <> struct ValueTraits<float> {
-    using Entry = uint2;
     using Bits = uint32_t;
     static constexpr int kPayloadWords = 1;
-    __device__ static inline Bits sym(const uint2 &e) { return e.x; }
-    __device__ static inline uint32_t meta(const uint2 &e) { return e.y; }
     __device__ static inline float from_bits(Bits b) { return __uint_as_float(b); }
     __device__ static inline float mul(float a, float b) { return __fmul_rn(a, b); }
     __device__ static inline float add(float a, float b) { return __fadd_rn(a, b); }
 };
 
 struct KernelArgs {
-    const uint2 *dtab;            // delta table (global copy)
-    const void *vtab;             // value table (global copy)
+    const uint32_t *tables;       // [dtab 4096][vtab 4096][ddict][vdict] (global copy)
+    int32_t table_bytes;          // bytes to copy into shared memory (multiple of 16)
+    int32_t off_ddict, off_vdict; // byte offsets inside the table block
+    uint32_t desc_min, vesc_min;  // entry >= this  <=>  escape (id == n_retained)
+    int32_t pads_ok;              // both domains retain a pad symbol
+    int32_t off_bars, off_meta, off_bufs;  // shared-memory layout
+    int32_t bufw;                 // words per stream buffer
     const uint32_t *row_symbols;  // rows
     const uint64_t *directory;    // nslices + 1
-    const uint32_t *stream;       // nwords (+ padding)
+    const uint32_t *stream;       // nwords (+ 64 B padding)
     int64_t rows, cols, nslices, nwords;
     const void *x;
-    const void *y;                // may be null
+    const void *y;                // may be null (y' = A x)
     void *out;
     const int64_t *row_start;     // decode kernel only
     int64_t *dec_cols;            // decode kernel only
     void *dec_vals;               // decode kernel only
     unsigned int *err;            // bit 0: consumption mismatch, bit 1: column OOB
-    int decode_only;
 };
 
 __device__ __forceinline__ uint32_t lanemask_lt()
@@ -82,228 +83,471 @@ __device__ __forceinline__ uint32_t lanemask_lt()
     return m;
 }
 
-__device__ __forceinline__ uint32_t ld_stream(const uint32_t *s, uint64_t pos)
+__device__ __forceinline__ uint32_t smem_u32(const void *p)
 {
-    return __ldg(s + pos);
+    return (uint32_t)__cvta_generic_to_shared(p);
 }
 
-template <typename V>
-__device__ __forceinline__ void decode_slice(const KernelArgs &a, const uint2 *__restrict__ sd,
-                                             const typename ValueTraits<V>::Entry *__restrict__ sv,
-                                             int64_t s, int lane)
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar)
+{
+    asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity)
+{
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar)
+{
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ void fence_proxy_async()
+{
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+__device__ __forceinline__ void fence_mbar_init()
+{
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ uint32_t lds32(uint32_t addr)
+{
+    uint32_t v;
+    asm("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+    return v;
+}
+
+__device__ __forceinline__ unsigned long long lds64(uint32_t addr)
+{
+    unsigned long long v;
+    asm("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(addr));
+    return v;
+}
+
+// Stream words that change between slices (TMA-written): volatile so they
+// are never hoisted across the mbarrier wait.
+__device__ __forceinline__ uint32_t lds32_v(uint32_t addr)
+{
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+    return v;
+}
+
+template <typename Bits> __device__ __forceinline__ Bits lds_bits(uint32_t addr);
+template <> __device__ __forceinline__ unsigned long long lds_bits<unsigned long long>(uint32_t addr)
+{
+    return lds64(addr);
+}
+template <> __device__ __forceinline__ uint32_t lds_bits<uint32_t>(uint32_t addr) { return lds32(addr); }
+
+// Word sources for one slice, addressed by the position relative to
+// directory[s] (32-bit): the staged shared-memory window or global memory.
+// Reads are not clamped: a segment consumes at most kSegMaxWords words, the
+// decoder stops as soon as its cursor passes the slice end (then reports
+// CorruptStream), and both the shared ring and the device stream carry at
+// least kOverrunWords of slack, so a corrupt container can never read
+// outside the allocations.
+constexpr uint32_t kSegMaxWords = 32u * 15u;  // payload 12 + 2 checks + 1 uncond per lane
+constexpr uint32_t kOverrunWords = 3u * 32u + kSegMaxWords + 64u;
+struct SmemSrc {
+    uint32_t addr;  // shared address of word directory[s]
+    __device__ __forceinline__ uint32_t operator()(uint32_t rel) const { return lds32_v(addr + rel * 4u); }
+};
+struct GmemSrc {
+    const uint32_t *p;  // &stream[directory[s]]
+    __device__ __forceinline__ uint32_t operator()(uint32_t rel) const { return __ldg(p + rel); }
+};
+
+// Per-buffer slice record written by the stager.
+struct SliceMeta {
+    uint32_t off;     // words from the 16-byte aligned window start to directory[s]
+    uint32_t nwords;  // directory[s+1] - directory[s]
+    uint32_t staged;  // 1: words are in the ring buffer
+    uint32_t pad;
+    uint64_t lo;      // directory[s]
+    uint64_t pad2;
+};
+
+// Stage slice s (whose directory entries lo, hi were prefetched) into a ring
+// buffer (lane 0 only).
+__device__ __forceinline__ void stage_slice(const KernelArgs &a, uint64_t lo, uint64_t hi, uint64_t *bar,
+                                            SliceMeta *meta, uint32_t *buf)
+{
+    const uint64_t abase = lo & ~3ull, aend = (hi + 3) & ~3ull;
+    const uint64_t bytes = (aend - abase) * 4;
+    const bool staged = bytes > 0 && bytes <= (uint64_t)a.bufw * 4;
+    meta->off = (uint32_t)(lo - abase);
+    meta->nwords = (uint32_t)(hi - lo);
+    meta->staged = staged ? 1u : 0u;
+    meta->lo = lo;
+    if (staged) {
+        mbar_arrive_expect_tx(bar, (uint32_t)bytes);
+        bulk_g2s(buf, a.stream + abase, (uint32_t)bytes, bar);
+    } else {
+        mbar_arrive(bar);
+    }
+}
+
+struct Ctx {
+    uint32_t dtab, vtab, ddict, vdict;  // shared addresses
+    uint32_t desc_min, vesc_min;        // entry >= this <=> escape
+    uint32_t cols_m1;
+    uint32_t lt;                        // lanemask_lt
+    bool pads_ok;
+};
+
+__device__ __forceinline__ void slot_offsets(uint32_t w0, uint32_t w1, uint32_t w2, uint32_t so[8])
+{
+    // unpack (codec.py:148-162): slot k = bits [12k, 12k+12) of w0:w1:w2, as
+    // byte offsets (slot * 4) into the u32 slot tables
+    so[0] = (w2 << 2) & 0x3FFCu;
+    so[1] = (w2 >> 10) & 0x3FFCu;
+    so[2] = __funnelshift_r(w2, w1, 22) & 0x3FFCu;
+    so[3] = (w1 >> 2) & 0x3FFCu;
+    so[4] = (w1 >> 14) & 0x3FFCu;
+    so[5] = __funnelshift_r(w1, w0, 26) & 0x3FFCu;
+    so[6] = (w0 >> 6) & 0x3FFCu;
+    so[7] = (w0 >> 18) & 0x3FFCu;
+}
+
+// Table entries of pair p and the dictionary symbols they point at (escape
+// entries point at a dummy dictionary slot; the payload overwrites them).
+template <typename Bits>
+__device__ __forceinline__ void lookup_pair(const Ctx &C, uint32_t sod, uint32_t sov, uint32_t &ed, uint32_t &ev,
+                                            uint32_t &ds, Bits &vs)
+{
+    ed = lds32(C.dtab + sod);
+    ev = lds32(C.vtab + sov);
+    ds = lds32(C.ddict + (ed >> 16));  // id field = byte offset into the dictionary
+    vs = lds_bits<Bits>(C.vdict + (ev >> 16));
+}
+
+// Payload event (container.py:459-470): per-lane word counts, exclusive warp
+// scan, words read in slot order, low word first, overwriting the symbols.
+template <typename T, class Src>
+__device__ __forceinline__ void payload_event(const Ctx &C, const Src &src, uint32_t &cur, const bool act,
+                                              const uint32_t e[8], uint32_t ds[4], typename T::Bits vs[4],
+                                              const int lane)
+{
+    using Bits = typename T::Bits;
+    uint32_t pc = 0;
+#pragma unroll
+    for (int p = 0; p < 4; p++)
+        pc += (e[2 * p] >= C.desc_min ? 1u : 0u) + (e[2 * p + 1] >= C.vesc_min ? (uint32_t)T::kPayloadWords : 0u);
+    if (!act) pc = 0;
+    const uint32_t any = __ballot_sync(0xFFFFFFFFu, pc != 0);
+    if (!any) return;
+    if (__all_sync(0xFFFFFFFFu, pc <= 1u)) {
+        // common case (e.g. one escaped first column per row): every lane
+        // reads at most one word, its rank among the escaping lanes
+        const uint32_t w = src(cur + __popc(any & C.lt));
+#pragma unroll
+        for (int p = 0; p < 4; p++) {
+            if (e[2 * p] >= C.desc_min) ds[p] = w;
+            if (T::kPayloadWords == 1 && e[2 * p + 1] >= C.vesc_min) vs[p] = (Bits)w;
+        }
+        cur += __popc(any);
+        return;
+    }
+    uint32_t incl = pc;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t v = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+        if (lane >= o) incl += v;
+    }
+    const uint32_t total = __shfl_sync(0xFFFFFFFFu, incl, 31);
+    if (pc) {
+        uint32_t off = cur + (incl - pc);
+#pragma unroll
+        for (int p = 0; p < 4; p++) {
+            if (e[2 * p] >= C.desc_min) {
+                ds[p] = src(off);
+                off += 1;
+            }
+            if (e[2 * p + 1] >= C.vesc_min) {
+                if (T::kPayloadWords == 2) {
+                    const uint32_t lo = src(off), hi = src(off + 1);
+                    vs[p] = (Bits)(((unsigned long long)hi << 32) | lo);
+                } else {
+                    vs[p] = (Bits)src(off);
+                }
+                off += T::kPayloadWords;
+            }
+        }
+    }
+    cur += total;
+}
+
+__device__ __forceinline__ uint32_t byte1(uint32_t x) { return __byte_perm(x, 0u, 0x4441u); }
+
+// Group of 4 slots -> decremented radix Bm1 = b0 b1 b2 b3 - 1 and digit D,
+// using b*x = bm1*x + x so no "+1" is needed (codec.py:127-137).
+__device__ __forceinline__ void group(uint32_t m0, uint32_t m1, uint32_t m2, uint32_t m3, uint32_t &bm1,
+                                      uint32_t &dg)
+{
+    const uint32_t q0 = byte1(m0), q1 = byte1(m1), q2 = byte1(m2), q3 = byte1(m3);
+    uint32_t P = q0 + 1u;       // b0
+    P = P * q1 + P;             // b0 b1
+    P = P * q2 + P;             // b0 b1 b2  (<= 2^24)
+    bm1 = P * q3 + (P - 1u);    // b0 b1 b2 b3 - 1
+    uint32_t D = m0 & 0xFFu;
+    D = D * q1 + (D + (m1 & 0xFFu));
+    D = D * q2 + (D + (m2 & 0xFFu));
+    dg = D * q3 + (D + (m3 & 0xFFu));
+}
+
+template <typename V, bool kDecode, bool kHasY, class Src>
+__device__ __forceinline__ void decode_slice(const KernelArgs &a, const Ctx &C, const V *__restrict__ x,
+                                             const Src src, const uint32_t end, const uint32_t n,
+                                             const uint32_t row, const bool inrow, const int lane)
 {
     using T = ValueTraits<V>;
     using Bits = typename T::Bits;
     const uint32_t FULL = 0xFFFFFFFFu;
-    const int64_t row = s * kSliceRows + lane;
-    const bool inrow = row < a.rows;
-    const uint32_t n = inrow ? __ldg(a.row_symbols + row) : 0u;
     const uint32_t nseg = (n + 7u) >> 3;
-    const uint32_t max_nseg = __reduce_max_sync(FULL, nseg);
-    uint64_t cur = __ldg(a.directory + s);
-    const uint64_t end = __ldg(a.directory + s + 1);
-    const uint64_t last_word = a.nwords > 0 ? (uint64_t)(a.nwords - 1) : 0;
-    const uint32_t lt = lanemask_lt();
-    const uint32_t *__restrict__ st = a.stream;
-
-    // init events: 3 words per active lane
-    uint32_t w0 = 0, w1 = 0, w2 = 0;
-    {
-        const uint32_t am = __ballot_sync(FULL, nseg > 0);
-        const uint32_t cnt = __popc(am), rk = __popc(am & lt);
-        if (nseg > 0) {
-            w0 = ld_stream(st, min(cur + rk, last_word));
-            w1 = ld_stream(st, min(cur + cnt + rk, last_word));
-            w2 = ld_stream(st, min(cur + 2 * cnt + rk, last_word));
-        }
-        cur += 3 * cnt;
-    }
-    uint32_t d = 0, r = 1;
-    uint32_t col = 0;
-    bool col_bad = false;
-    V acc = V(0);
+    const uint32_t maxn = __reduce_max_sync(FULL, n);
+    const uint32_t max_nseg = (maxn + 7u) >> 3;
+    V yv = V(0);
+    if (kHasY) yv = __ldg(reinterpret_cast<const V *>(a.y) + (inrow ? row : 0u));
     int64_t out_pos = 0;
-    if (a.decode_only && inrow) out_pos = a.row_start[row];
+    if (kDecode && inrow) out_pos = __ldg(a.row_start + row);
 
-    for (uint32_t j = 0; j < max_nseg; j++) {
+    // init events (container.py:426-429): 3 words per active lane
+    uint32_t w0 = 0, w1 = 0, w2 = 0, cur;
+    {
+        const uint32_t am = __ballot_sync(FULL, n > 0);
+        const uint32_t cnt = __popc(am), rk = __popc(am & C.lt);
+        if (n > 0) {
+            w0 = src(rk);
+            w1 = src(cnt + rk);
+            w2 = src(2 * cnt + rk);
+        }
+        cur = 3 * cnt;
+    }
+    uint32_t d = 0, r = 1, col = 0;
+    V acc = V(0);
+    bool bad = false;
+
+    // Segments where some lane still folds digits: all 8 slots, radix chain.
+    for (uint32_t j = 0; j + 1 < max_nseg; j++) {  // (max_nseg == 0: no iterations)
         const bool act = j < nseg;
         const bool notlast = j + 1 < nseg;
-        // unpack (codec.py:148-162): slot k = bits [12k, 12k+12) of w0:w1:w2
-        uint32_t sl[8];
-        sl[0] = w2 & 0xFFFu;
-        sl[1] = (w2 >> 12) & 0xFFFu;
-        sl[2] = __funnelshift_r(w2, w1, 24) & 0xFFFu;
-        sl[3] = (w1 >> 4) & 0xFFFu;
-        sl[4] = (w1 >> 16) & 0xFFFu;
-        sl[5] = __funnelshift_r(w1, w0, 28) & 0xFFFu;
-        sl[6] = (w0 >> 8) & 0xFFFu;
-        sl[7] = w0 >> 20;
-        uint2 de[4];
-        typename T::Entry ve[4];
+        uint32_t so[8], e[8], ds[4];
+        Bits vs[4];
+        slot_offsets(w0, w1, w2, so);
+#pragma unroll
+        for (int p = 0; p < 4; p++) lookup_pair<Bits>(C, so[2 * p], so[2 * p + 1], e[2 * p], e[2 * p + 1], ds[p], vs[p]);
+        payload_event<T>(C, src, cur, act, e, ds, vs, lane);
+        V xv[4];
 #pragma unroll
         for (int p = 0; p < 4; p++) {
-            de[p] = sd[sl[2 * p]];
-            ve[p] = sv[sl[2 * p + 1]];
-        }
-        uint32_t dsym[4];
-        Bits vsym[4];
-        uint32_t dmeta[4], vmeta[4];
-        uint32_t pc = 0;
-#pragma unroll
-        for (int p = 0; p < 4; p++) {
-            dsym[p] = de[p].x;
-            dmeta[p] = de[p].y;
-            vsym[p] = T::sym(ve[p]);
-            vmeta[p] = T::meta(ve[p]);
-            pc += (dmeta[p] >> 16) & 1u;
-            pc += ((vmeta[p] >> 16) & 1u) * T::kPayloadWords;
-        }
-        if (!act) pc = 0;
-        // payload event (container.py:459-470): exclusive scan of counts
-        if (__any_sync(FULL, pc != 0)) {
-            uint32_t incl = pc;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t v = __shfl_up_sync(FULL, incl, o);
-                if (lane >= o) incl += v;
-            }
-            const uint32_t total = __shfl_sync(FULL, incl, 31);
-            uint64_t off = cur + (incl - pc);
-            if (pc) {
-#pragma unroll
-                for (int p = 0; p < 4; p++) {
-                    if ((dmeta[p] >> 16) & 1u) {
-                        dsym[p] = ld_stream(st, min(off, last_word));
-                        off += 1;
-                    }
-                    if ((vmeta[p] >> 16) & 1u) {
-                        if (T::kPayloadWords == 2) {
-                            const uint32_t lo = ld_stream(st, min(off, last_word));
-                            const uint32_t hi = ld_stream(st, min(off + 1, last_word));
-                            vsym[p] = (Bits)(((unsigned long long)hi << 32) | lo);
-                        } else {
-                            vsym[p] = (Bits)ld_stream(st, min(off, last_word));
-                        }
-                        off += T::kPayloadWords;
-                    }
-                }
-            }
-            cur += total;
-        }
-        // mixed-radix checks: bases only decide load vs extract
-        uint32_t bm1g[2], dg[2];
-#pragma unroll
-        for (int g = 0; g < 2; g++) {
-            // positions 4g..4g+3: delta, value, delta, value
-            const uint32_t m0 = dmeta[2 * g], m1 = vmeta[2 * g];
-            const uint32_t m2 = dmeta[2 * g + 1], m3 = vmeta[2 * g + 1];
-            const uint32_t b0 = ((m0 >> 8) & 0xFFu) + 1u, b1 = ((m1 >> 8) & 0xFFu) + 1u;
-            const uint32_t b2 = ((m2 >> 8) & 0xFFu) + 1u, b3m1 = (m3 >> 8) & 0xFFu;
-            const uint32_t P = b0 * b1 * b2;                      // <= 2^24
-            bm1g[g] = P * b3m1 + (P - 1u);                         // b0 b1 b2 b3 - 1
-            dg[g] = (((m0 & 0xFFu) * b1 + (m1 & 0xFFu)) * b2 + (m2 & 0xFFu)) * (b3m1 + 1u) +
-                    (m3 & 0xFFu);
-        }
-        // radix chain (depends on bases only) -> load flags of both checks
-        const unsigned long long r1 = (unsigned long long)r * bm1g[0] + r;
-        const bool ext0 = (r1 >> 32) != 0;
-        const uint32_t ra = ext0 ? (uint32_t)(r1 >> 32) : (uint32_t)r1;
-        const unsigned long long r2 = (unsigned long long)ra * bm1g[1] + ra;
-        const bool ext1 = (r2 >> 32) != 0;
-        const bool ld0 = notlast && !ext0, ld1 = notlast && !ext1;
-        const uint32_t m_ld0 = __ballot_sync(FULL, ld0);
-        const uint32_t m_ld1 = __ballot_sync(FULL, ld1);
-        const uint32_t m_nl = __ballot_sync(FULL, notlast);
-        const uint64_t p0 = cur + __popc(m_ld0 & lt);
-        const uint64_t c1 = cur + __popc(m_ld0);
-        const uint64_t p1 = c1 + __popc(m_ld1 & lt);
-        const uint64_t c2 = c1 + __popc(m_ld1);
-        const uint64_t p2 = c2 + __popc(m_nl & lt);
-        cur = c2 + __popc(m_nl);
-        uint32_t lw0 = 0, lw1 = 0, lw2 = 0;
-        if (ld0) lw0 = ld_stream(st, min(p0, last_word));
-        if (ld1) lw1 = ld_stream(st, min(p1, last_word));
-        if (notlast) lw2 = ld_stream(st, min(p2, last_word));
-
-        // symbols of this segment -> columns, values, products
-#pragma unroll
-        for (int p = 0; p < 4; p++) {
-            const bool valid = act && (8u * j + 2u * p) < n;
-            if (valid) {
-                col += dsym[p];
-                const bool oob = col >= (uint64_t)a.cols;
-                col_bad |= oob;
-                const uint32_t c = oob ? 0u : col;
-                if (a.decode_only) {
+            xv[p] = V(0);
+            if (8u * j + 2u * p < n) {
+                col += ds[p];
+                if (kDecode) {
                     a.dec_cols[out_pos] = (int64_t)col;
-                    reinterpret_cast<Bits *>(a.dec_vals)[out_pos] = vsym[p];
+                    reinterpret_cast<Bits *>(a.dec_vals)[out_pos] = vs[p];
                     out_pos++;
                 } else {
-                    const V xv = __ldg(reinterpret_cast<const V *>(a.x) + c);
-                    acc = T::add(acc, T::mul(T::from_bits(vsym[p]), xv));
+                    xv[p] = __ldg(x + min(col, C.cols_m1));
                 }
             }
         }
-        // digit chain
+        // mixed-radix checks (container.py:478-497): bases decide load vs extract
+        uint32_t bm1a, dga, bm1b, dgb;
+        group(e[0], e[1], e[2], e[3], bm1a, dga);
+        group(e[4], e[5], e[6], e[7], bm1b, dgb);
+        const unsigned long long r1 = (unsigned long long)r * bm1a + r;
+        const uint32_t r1h = (uint32_t)(r1 >> 32);
+        const bool ext0 = r1h != 0u;
+        const uint32_t ra = ext0 ? r1h : (uint32_t)r1;
+        const unsigned long long r2 = (unsigned long long)ra * bm1b + ra;
+        const uint32_t r2h = (uint32_t)(r2 >> 32);
+        const bool ext1 = r2h != 0u;
+        const uint32_t m_ld0 = __ballot_sync(FULL, notlast && !ext0);
+        const uint32_t m_ld1 = __ballot_sync(FULL, notlast && !ext1);
+        const uint32_t m_nl = __ballot_sync(FULL, notlast);
+        const uint32_t c1 = cur + __popc(m_ld0);
+        const uint32_t c2 = c1 + __popc(m_ld1);
+        const uint32_t lw0 = src(cur + __popc(m_ld0 & C.lt));
+        const uint32_t lw1 = src(c1 + __popc(m_ld1 & C.lt));
+        const uint32_t lw2 = src(c2 + __popc(m_nl & C.lt));
+        cur = c2 + __popc(m_nl);
         if (notlast) {
-            const unsigned long long d1 =
-                (unsigned long long)d * bm1g[0] + ((unsigned long long)d + dg[0]);
-            uint32_t da;
-            if (ext0) {
-                w0 = (uint32_t)d1;
-                da = (uint32_t)(d1 >> 32);
-            } else {
-                w0 = lw0;
-                da = (uint32_t)d1;
-            }
-            const unsigned long long d2 =
-                (unsigned long long)da * bm1g[1] + ((unsigned long long)da + dg[1]);
-            if (ext1) {
-                w1 = (uint32_t)d2;
-                d = (uint32_t)(d2 >> 32);
-                r = (uint32_t)(r2 >> 32);
-            } else {
-                w1 = lw1;
-                d = (uint32_t)d2;
-                r = (uint32_t)r2;
-            }
+            const unsigned long long d1 = (unsigned long long)d * bm1a + ((unsigned long long)d + dga);
+            const uint32_t da = ext0 ? (uint32_t)(d1 >> 32) : (uint32_t)d1;
+            w0 = ext0 ? (uint32_t)d1 : lw0;
+            const unsigned long long d2 = (unsigned long long)da * bm1b + ((unsigned long long)da + dgb);
+            w1 = ext1 ? (uint32_t)d2 : lw1;
+            d = ext1 ? (uint32_t)(d2 >> 32) : (uint32_t)d2;
+            r = ext1 ? r2h : (uint32_t)r2;
             w2 = lw2;
+        }
+        if (!kDecode) {
+#pragma unroll
+            for (int p = 0; p < 4; p++)
+                if (8u * j + 2u * p < n) acc = T::add(acc, T::mul(T::from_bits(vs[p]), xv[p]));
+        }
+        if (cur > end) {  // uniform: corrupt slice, stop before reading further
+            bad = true;
+            break;
+        }
+    }
+    // Final segment: every active lane is in its last segment, so no digits
+    // are folded and no checks/unconditional loads happen; pairs past the
+    // longest row are skipped (pads need lookups only when they may escape).
+    if (max_nseg > 0 && !bad) {
+        const uint32_t j = max_nseg - 1;
+        const bool act = j < nseg;
+        uint32_t so[8], e[8], ds[4];
+        Bits vs[4];
+        slot_offsets(w0, w1, w2, so);
+        const uint32_t base = 8u * j;
+#pragma unroll
+        for (int p = 0; p < 4; p++) {
+            if (!C.pads_ok || base + 2u * p < maxn) {  // uniform
+                lookup_pair<Bits>(C, so[2 * p], so[2 * p + 1], e[2 * p], e[2 * p + 1], ds[p], vs[p]);
+            } else {
+                e[2 * p] = e[2 * p + 1] = 0u;
+                ds[p] = 0u;
+                vs[p] = 0;
+            }
+        }
+        payload_event<T>(C, src, cur, act, e, ds, vs, lane);
+#pragma unroll
+        for (int p = 0; p < 4; p++) {
+            if (base + 2u * p < maxn) {  // uniform
+                if (base + 2u * p < n) {
+                    col += ds[p];
+                    if (kDecode) {
+                        a.dec_cols[out_pos] = (int64_t)col;
+                        reinterpret_cast<Bits *>(a.dec_vals)[out_pos] = vs[p];
+                        out_pos++;
+                    } else {
+                        const V xv = __ldg(x + min(col, C.cols_m1));
+                        acc = T::add(acc, T::mul(T::from_bits(vs[p]), xv));
+                    }
+                }
+            }
         }
     }
     if (lane == 0 && cur != end) atomicOr(a.err, 1u);
-    if (__any_sync(FULL, col_bad) && lane == 0) atomicOr(a.err, 2u);
-    if (!a.decode_only && inrow) {
-        V res = acc;
-        if (a.y) res = T::add(acc, reinterpret_cast<const V *>(a.y)[row]);
+    if (__any_sync(FULL, n > 0 && col > C.cols_m1) && lane == 0) atomicOr(a.err, 2u);
+    if (!kDecode && inrow) {
+        const V res = kHasY ? T::add(acc, yv) : acc;
         reinterpret_cast<V *>(a.out)[row] = res;
     }
 }
 
-// Persistent kernel: tables -> shared memory once per CTA, then every warp
-// walks slices with a grid-wide stride.
-template <typename V>
-__global__ void __launch_bounds__(512, 1) dtans_spmv_kernel(KernelArgs a)
+// Persistent kernel, one CTA of 32 warps per SM: tables -> shared memory once,
+// then every warp walks its slices (grid-wide stride) through its TMA ring.
+template <typename V, bool kDecode, bool kHasY, int kThreads>
+__global__ void __launch_bounds__(kThreads, 1) dtans_kernel(const KernelArgs a)
 {
-    using Entry = typename ValueTraits<V>::Entry;
-    extern __shared__ __align__(16) unsigned char smem[];
-    uint2 *sd = reinterpret_cast<uint2 *>(smem);
-    Entry *sv = reinterpret_cast<Entry *>(smem + kSlots * sizeof(uint2));
+    constexpr int kWarps = kThreads / 32;
+    extern __shared__ __align__(128) unsigned char smem[];
     {
-        const int4 *src = reinterpret_cast<const int4 *>(a.dtab);
-        int4 *dst = reinterpret_cast<int4 *>(sd);
-        for (int i = threadIdx.x; i < kSlots * (int)sizeof(uint2) / 16; i += blockDim.x)
-            dst[i] = __ldg(src + i);
-        const int4 *vsrc = reinterpret_cast<const int4 *>(a.vtab);
-        int4 *vdst = reinterpret_cast<int4 *>(sv);
-        for (int i = threadIdx.x; i < kSlots * (int)sizeof(Entry) / 16; i += blockDim.x)
-            vdst[i] = __ldg(vsrc + i);
+        const int4 *srcv = reinterpret_cast<const int4 *>(a.tables);
+        int4 *dst = reinterpret_cast<int4 *>(smem);
+        for (int i = threadIdx.x; i < a.table_bytes / 16; i += blockDim.x) dst[i] = __ldg(srcv + i);
+    }
+    const uint32_t sbase = smem_u32(smem);
+    Ctx C;
+    C.dtab = sbase;
+    C.vtab = sbase + kSlots * 4;
+    C.ddict = sbase + (uint32_t)a.off_ddict;
+    C.vdict = sbase + (uint32_t)a.off_vdict;
+    C.desc_min = a.desc_min;
+    C.vesc_min = a.vesc_min;
+    C.cols_m1 = (uint32_t)(a.cols - 1);
+    C.lt = lanemask_lt();
+    C.pads_ok = a.pads_ok != 0;
+    const V *__restrict__ x = reinterpret_cast<const V *>(a.x);
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smem + a.off_bars) + warp * kRing;
+    SliceMeta *meta = reinterpret_cast<SliceMeta *>(smem + a.off_meta) + warp * kRing;
+    uint32_t *bufs = reinterpret_cast<uint32_t *>(smem + a.off_bufs) + (size_t)warp * kRing * a.bufw;
+    if (lane == 0) {
+        for (int b = 0; b < kRing; b++) mbar_init(&bars[b], 1);
+        fence_mbar_init();
     }
     __syncthreads();
-    const int lane = threadIdx.x & 31;
-    const int warps = blockDim.x >> 5;
-    const int64_t gw = (int64_t)blockIdx.x * warps + (threadIdx.x >> 5);
-    const int64_t stride = (int64_t)gridDim.x * warps;
-    for (int64_t s = gw; s < a.nslices; s += stride) decode_slice<V>(a, sd, sv, s, lane);
+
+    const uint32_t nsl = (uint32_t)a.nslices;
+    const uint32_t rows = (uint32_t)a.rows;  // < 2^32 (checked at upload)
+    const uint32_t first = blockIdx.x * kWarps + warp;
+    const uint32_t stride = gridDim.x * kWarps;
+    if (lane == 0)
+        for (int b = 0; b < kRing; b++) {
+            const uint32_t s = first + b * stride;
+            if (s < nsl)
+                stage_slice(a, __ldg(a.directory + s), __ldg(a.directory + s + 1), &bars[b], &meta[b],
+                            bufs + b * a.bufw);
+        }
+    uint32_t n_next = 0;
+    if (first < nsl && first * kSliceRows + lane < rows) n_next = __ldg(a.row_symbols + first * kSliceRows + lane);
+    int b = 0;
+    uint32_t parity = 0;
+    for (uint32_t s = first; s < nsl; s += stride) {
+        const uint32_t n = n_next;
+        const uint32_t sn = s + stride;
+        n_next = (sn < nsl && sn * kSliceRows + lane < rows) ? __ldg(a.row_symbols + sn * kSliceRows + lane) : 0u;
+        // directory entries of the slice this buffer is refilled with
+        const uint32_t sr = s + kRing * stride;
+        uint64_t rlo = 0, rhi = 0;
+        if (lane == 0 && sr < nsl) {
+            rlo = __ldg(a.directory + sr);
+            rhi = __ldg(a.directory + sr + 1);
+        }
+        mbar_wait(&bars[b], parity);
+        const SliceMeta md = meta[b];
+        const uint32_t row = s * kSliceRows + lane;
+        const bool inrow = row < rows;
+        if (md.staged) {
+            const SmemSrc src{smem_u32(bufs + b * a.bufw) + md.off * 4u};
+            decode_slice<V, kDecode, kHasY>(a, C, x, src, md.nwords, n, row, inrow, lane);
+        } else {
+            const GmemSrc src{a.stream + md.lo};
+            decode_slice<V, kDecode, kHasY>(a, C, x, src, md.nwords, n, row, inrow, lane);
+        }
+        __syncwarp();
+        if (lane == 0 && sr < nsl) {
+            fence_proxy_async();
+            stage_slice(a, rlo, rhi, &bars[b], &meta[b], bufs + b * a.bufw);
+        }
+        if (++b == kRing) {
+            b = 0;
+            parity ^= 1u;
+        }
+    }
 }
 
 }  // namespace dev

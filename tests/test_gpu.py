@@ -46,7 +46,7 @@ def test_spmv_from_reference_bytes(name):
 
 def test_corrupt_directory_raises():
     rec = G.load("laplacian_g48")
-    c = P.deserialize(rec["container"].tobytes())
+    c = P.encode_matrix(G.matrix(rec))
     d = c.directory.copy()
     d[1:-1] += 1  # every slice boundary shifted by one word
     c.directory = d
