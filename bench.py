@@ -1,0 +1,422 @@
+"""Benchmark: fused dtANS decode + SpMV on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl dtans|reference]
+                    [--config laplacian|config1|banded27|rmat|banded32] [--scale S]
+
+A "step" is one y' = A x + y over the whole synthetic matrix (one pass of the
+hot path over one batch).  N=1 default workload: BASELINE.json configs[1],
+the 2D 5-point Laplacian with 2^25 nnz (g=2591), fp64.  For N>1 (torchrun,
+one rank per GPU) the matrix is the Laplacian of an (N*g) x g grid,
+row-partitioned into N slabs; each rank encodes and decodes only its own slab
+(weak scaling, no data-path collective).
+
+Printed JSON (rank 0): value = whole-job GFLOP/s (2*nnz/t) with inputs
+resident in HBM; e2e = the same through the C-ABI host-buffer entry point
+(pinned x/y/out copied every step); roofline = algorithmic HBM bytes of the
+fused kernel / its CUDA-event time vs MEASURED_PEAKS.json; cpu_baseline =
+the oracle C port of the reference decode+SpMV on the host cores;
+cusparse_csr = torch.addmv (cuSPARSE CSR) on the same matrix and vectors.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+PEAKS_FALLBACK = {"hbm_gbs": 6650.0}
+
+
+def peaks():
+    p = os.path.join(REPO, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return d, "measured"
+    except Exception:
+        return PEAKS_FALLBACK, "fallback"
+
+
+def build_matrix(config: str, scale: float, world: int, rank: int):
+    """Synthetic matrix for this rank (row slab of the global matrix)."""
+    from paper_2603_01915_b200 import synth
+    from paper_2603_01915_b200.sparse import CsrMatrix
+    if config == "laplacian":
+        g = max(8, int(round(2591 * scale)))
+        if world == 1:
+            return synth.laplacian_2d(g), {"workload": "2D 5-point Laplacian, BASELINE configs[1]",
+                                           "grid": [g, g]}
+        # (world*g) x g grid: rank r owns grid rows [r*g, (r+1)*g)
+        m = _laplacian_slab(g, world, rank)
+        return m, {"workload": "2D 5-point Laplacian slab (weak scaling)", "grid": [world * g, g]}
+    if config == "config1":
+        return synth.config1_random(), {"workload": "random 4096x4096 2^15 nnz, BASELINE configs[0]"}
+    if config == "banded27":
+        rows = int(-(-2**28 // 27) * scale)
+        return synth.banded(rows, 27), {"workload": "banded-27 256-level alphabet, BASELINE configs[3]"}
+    if config == "banded32":
+        rows = int(2**24 * scale)
+        return synth.banded(rows, 32, positive=True), {"workload": "banded-32 positive alphabet, BASELINE configs[4]"}
+    if config == "rmat":
+        sc = 23 if scale >= 1 else max(10, int(round(23 + np.log2(scale))))
+        return synth.rmat(sc, int(2**27 * min(scale, 1.0) if sc == 23 else 16 << sc)), {
+            "workload": "R-MAT power-law fp32, BASELINE configs[2]"}
+    raise SystemExit(f"unknown config {config}")
+
+
+def _laplacian_slab(g: int, world: int, rank: int):
+    from paper_2603_01915_b200.sparse import CsrMatrix
+    G = world * g  # grid rows
+    n_all = G * g
+    r0, r1 = rank * g * g, (rank + 1) * g * g
+    i = np.arange(r0, r1, dtype=np.int64)
+    a, b = np.divmod(i, g)
+    offs = np.array([-g, -1, 0, 1, g], dtype=np.int64)
+    valid = np.stack([a > 0, b > 0, np.ones(len(i), bool), b < g - 1, a < G - 1], axis=1)
+    cols = i[:, None] + offs[None, :]
+    vals = np.broadcast_to(np.where(offs == 0, 4.0, -1.0), (len(i), 5))
+    row_start = np.zeros(len(i) + 1, dtype=np.int64)
+    np.cumsum(valid.sum(axis=1), out=row_start[1:])
+    return CsrMatrix(len(i), n_all, row_start, cols[valid], np.ascontiguousarray(vals[valid]))
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled while the timed region runs."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap,utilization.gpu")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for k, v in zip(names, f[4:8]):
+                if v.lower() in ("active", "1"):
+                    reasons.add(k)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": mx, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def dist_setup(gpus: int):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl")
+    return world, rank, local
+
+
+def max_over_ranks(v: float, world: int, device) -> float:
+    if world == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([v], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def sum_over_ranks(v: float, world: int, device) -> float:
+    if world == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([v], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
+
+
+def barrier(world: int):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def cpu_reference(args, world, rank):
+    """--impl reference: the reference algorithm on the host (oracle C port),
+    all host threads, same metric/config."""
+    if rank != 0:
+        return
+    import paper_2603_01915_b200 as P
+    from oracle import oracle as O
+    m, cfg = build_matrix(args.config, args.scale, 1, 0)
+    c = P.encode_matrix(m)
+    oc = O.parse(P.serialize(c))
+    from paper_2603_01915_b200 import synth
+    x, y = synth.vectors(m)
+    threads = os.cpu_count() or 1
+    for _ in range(args.warmup):
+        O.spmv(oc, x, y, threads=threads)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        O.spmv(oc, x, y, threads=threads)
+    t = (time.perf_counter() - t0) / args.steps
+    val = 2 * m.nnz / t / 1e9
+    cfg.update({"rows": m.rows, "nnz": m.nnz, "precision": "f64" if c.precision == 8 else "f32"})
+    out = {"metric": "dtANS SpMV GFLOP/s (2*nnz/t)", "value": val, "unit": "GFLOP/s", "n_gpus": world,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+           "scaling": "weak", "vs_baseline": None, "dtype": "u32 decode + f64 FMA" if c.precision == 8 else "u32 decode + f32",
+           "data": "synthetic", "config": cfg, "impl": "reference",
+           "cpu_baseline": {"value": val, "unit": "GFLOP/s", "cores": threads, "kind": "port",
+                            "sample": "full matrix per step (oracle/dtans_oracle.c, restating container.py:370-596)"},
+           "e2e": {"value": val, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="dtans", choices=["dtans", "reference"])
+    ap.add_argument("--config", default="laplacian")
+    ap.add_argument("--scale", type=float, default=1.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-cusparse", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+
+    world, rank, local = dist_setup(args.gpus)
+    if args.impl == "reference":
+        cpu_reference(args, world, rank)
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+        return
+
+    import torch
+
+    import paper_2603_01915_b200 as P
+    from paper_2603_01915_b200 import synth
+    from paper_2603_01915_b200.sparse import format_size_bytes
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    t0 = time.time()
+    m, cfg = build_matrix(args.config, args.scale, world, rank)
+    t_gen = time.time() - t0
+    t0 = time.time()
+    c = P.encode_matrix(m)
+    t_enc = time.time() - t0
+    x, y = synth.vectors(m)
+    V = np.float64 if c.precision == 8 else np.float32
+    esz = c.precision
+    dc = c.device(local)
+    xt = torch.from_numpy(x).to(dev)
+    yt = torch.from_numpy(y).to(dev)
+    out = torch.empty_like(yt)
+    stream = torch.cuda.current_stream(dev)
+
+    # correctness gate on this exact workload (decoded result vs inputs is
+    # covered by tests; here: the kernel flags no corrupt slice)
+    for _ in range(args.warmup):
+        dc.spmv(xt, yt, out)
+    dc.check()
+
+    size = P.size_bytes(c)
+    alg_bytes = size + esz * m.cols + 2 * esz * m.rows  # container + x + y + y'
+    L2 = torch.cuda.get_device_properties(dev).L2_cache_size
+    launches0 = dc.launches()
+    with ClockSampler(local) as clk:
+        time.sleep(0.15)
+        barrier(world)
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            dc.spmv(xt, yt, out)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        gpu_launches = dc.launches() - launches0
+        barrier(world)
+        # keep the GPU busy long enough for the sampler to see the clocks
+        t_end = time.time() + max(0.0, 0.6 - e0.elapsed_time(e1) / 1e3)
+        while time.time() < t_end:
+            for _ in range(50):
+                dc.spmv(xt, yt, out)
+            torch.cuda.synchronize()
+    ms_local = e0.elapsed_time(e1) / args.steps
+    dc.check()
+    ms = max_over_ranks(ms_local, world, dev)
+    nnz_total = sum_over_ranks(float(m.nnz), world, dev)
+    value = 2 * nnz_total / (ms * 1e-3) / 1e9
+
+    # cold-L2 kernel time: flush (write > L2) before every launch
+    flush = torch.empty(2 * L2, dtype=torch.uint8, device=dev)
+    cold = []
+    for _ in range(min(20, max(5, args.steps // 10))):
+        flush.fill_(1)
+        a0 = torch.cuda.Event(enable_timing=True)
+        a1 = torch.cuda.Event(enable_timing=True)
+        a0.record(stream)
+        dc.spmv(xt, yt, out)
+        a1.record(stream)
+        torch.cuda.synchronize()
+        cold.append(a0.elapsed_time(a1))
+    del flush
+    ms_cold = statistics.median(cold)
+
+    # end to end through the C ABI with pinned host buffers (copies inside)
+    xh = torch.from_numpy(x).pin_memory().numpy()
+    yh = torch.from_numpy(y).pin_memory().numpy()
+    oh = torch.empty(m.rows, dtype=torch.float64 if esz == 8 else torch.float32).pin_memory().numpy()
+    for _ in range(2):
+        dc.spmv_host(xh, yh, oh)
+    e2e_steps = max(3, min(args.steps, 50))
+    barrier(world)
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        dc.spmv_host(xh, yh, oh)
+    e2e_ms_local = (time.perf_counter() - t0) / e2e_steps * 1e3
+    e2e_ms = max_over_ranks(e2e_ms_local, world, dev)
+    e2e_val = 2 * nnz_total / (e2e_ms * 1e-3) / 1e9
+    ref_ok = bool(np.array_equal(oh.view(np.uint8), out.cpu().numpy().view(np.uint8)))
+
+    # cuSPARSE CSR comparator (torch.addmv on a sparse CSR tensor)
+    cus = None
+    if not args.no_cusparse:
+        try:
+            import warnings
+            warnings.filterwarnings("ignore")
+            A = torch.sparse_csr_tensor(torch.from_numpy(m.row_start), torch.from_numpy(m.col_idx),
+                                        torch.from_numpy(np.asarray(m.values, dtype=V)), size=(m.rows, m.cols)).to(dev)
+            for _ in range(3):
+                torch.addmv(yt, A, xt)
+            torch.cuda.synchronize()
+            b0 = torch.cuda.Event(enable_timing=True)
+            b1 = torch.cuda.Event(enable_timing=True)
+            ns = max(10, args.steps)
+            b0.record(stream)
+            for _ in range(ns):
+                torch.addmv(yt, A, xt)
+            b1.record(stream)
+            torch.cuda.synchronize()
+            cms = max_over_ranks(b0.elapsed_time(b1) / ns, world, dev)
+            csr_bytes = format_size_bytes(m, "csr", esz) + esz * m.cols + 2 * esz * m.rows
+            cus = {"impl": "torch.addmv sparse_csr (cuSPARSE SpMV)", "ms": cms,
+                   "value": 2 * nnz_total / (cms * 1e-3) / 1e9, "unit": "GFLOP/s",
+                   "dtans_speedup": cms / ms, "csr_algorithmic_gbs": csr_bytes / (cms * 1e-3) / 1e9 * world}
+            del A
+        except Exception as e:  # comparator only
+            cus = {"error": str(e)[:200]}
+
+    pk, pk_kind = peaks()
+    achieved = alg_bytes / (ms_local * 1e-3) / 1e9
+    traffic = None
+    tpath = os.path.join(REPO, "profiles", f"traffic_{args.config}.json")
+    if os.path.exists(tpath) and world == 1 and args.scale == 1.0:
+        try:
+            traffic = json.load(open(tpath)).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    comp = min(format_size_bytes(m, f, esz) for f in ("csr", "coo", "sell")) / size
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(c, x, y)
+
+    info = dc.info()
+    cfg.update({"rows": m.rows, "cols": m.cols, "nnz": m.nnz, "precision": "f64" if esz == 8 else "f32",
+                "parallelism": f"row-slab x{world}" if world > 1 else "1 GPU",
+                "l2": f"working set {alg_bytes / L2:.1f}x L2 (no flush between steps); cold-L2 time in cold_ms",
+                "container_bytes": size, "compression_vs_min_csr_coo_sell": comp,
+                "encode_s": t_enc, "generate_s": t_gen, "launch": info})
+    res = {
+        "metric": "dtANS SpMV GFLOP/s (2*nnz/t)", "value": value, "unit": "GFLOP/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None,
+        "dtype": "u32 decode + f64 FMA" if esz == 8 else "u32 decode + f32 FMA",
+        "data": "synthetic", "config": cfg,
+        "effective_gbs": alg_bytes / (ms * 1e-3) / 1e9 * world, "container_gbs": size / (ms * 1e-3) / 1e9 * world,
+        "cold_ms": ms_cold,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                     "frac": achieved / pk["hbm_gbs"], "traffic": traffic,
+                     "peak_kind": pk_kind, "algorithmic_bytes_per_launch": alg_bytes,
+                     "kernel": "dtans_kernel<double,false,true,*> (fused decode+SpMV)"},
+        "e2e": {"value": e2e_val, "unit": "GFLOP/s", "ms_per_step": e2e_ms,
+                "h2d_bytes_per_step": esz * (m.cols + m.rows), "d2h_bytes_per_step": esz * m.rows,
+                "path": "dtans_spmv_host (C ABI, pinned host x/y/out)", "matches_device_result": ref_ok},
+        "cusparse_csr": cus,
+        "cpu_baseline": cpu,
+        "clocks": clk.summary(),
+        "gpu_launches": gpu_launches,
+    }
+    if rank == 0:
+        print(json.dumps(res), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+def cpu_baseline(c, x, y):
+    """Oracle C port of the reference decode+SpMV on the host cores, a
+    bounded sample (~10 s): repeated full-matrix SpMVs with all threads."""
+    import paper_2603_01915_b200 as P
+    from oracle import oracle as O
+    oc = O.parse(P.serialize(c))
+    threads = os.cpu_count() or 1
+    O.spmv(oc, x, y, threads=threads)
+    reps, t_total = 0, 0.0
+    while t_total < 8.0 and reps < 50:
+        t0 = time.perf_counter()
+        O.spmv(oc, x, y, threads=threads)
+        t_total += time.perf_counter() - t0
+        reps += 1
+    t = t_total / reps
+    return {"value": 2 * c.nnz / t / 1e9, "unit": "GFLOP/s", "cores": threads, "kind": "port",
+            "sample": f"{reps} full-matrix SpMVs ({t * 1e3:.1f} ms each), oracle/dtans_oracle.c"}
+
+
+if __name__ == "__main__":
+    main()

@@ -185,31 +185,29 @@ struct GmemSrc {
     __device__ __forceinline__ uint32_t operator()(uint32_t rel) const { return __ldg(p + rel); }
 };
 
-// Per-buffer slice record written by the stager.
+// Per-buffer slice record written by the stager: the slice's word offset
+// inside the 16-byte aligned staged window (bit 31: not staged, read from
+// global memory instead) and its word count.
 struct SliceMeta {
-    uint32_t off;     // words from the 16-byte aligned window start to directory[s]
+    uint32_t off;     // words from the window start to directory[s]; bit 31 = global
     uint32_t nwords;  // directory[s+1] - directory[s]
-    uint32_t staged;  // 1: words are in the ring buffer
-    uint32_t pad;
-    uint64_t lo;      // directory[s]
-    uint64_t pad2;
 };
+constexpr uint32_t kGlobalSlice = 0x80000000u;
 
-// Stage slice s (whose directory entries lo, hi were prefetched) into a ring
-// buffer (lane 0 only).
+// Stage a slice (directory entries lo, hi prefetched) into a ring buffer
+// (lane 0 only).  The previous contents were consumed by this warp's LDS
+// before the __syncwarp that precedes the call (the same WAR ordering a
+// CUTLASS TMA pipeline relies on), so no proxy fence is issued.
 __device__ __forceinline__ void stage_slice(const KernelArgs &a, uint64_t lo, uint64_t hi, uint64_t *bar,
                                             SliceMeta *meta, uint32_t *buf)
 {
-    const uint64_t abase = lo & ~3ull, aend = (hi + 3) & ~3ull;
-    const uint64_t bytes = (aend - abase) * 4;
-    const bool staged = bytes > 0 && bytes <= (uint64_t)a.bufw * 4;
-    meta->off = (uint32_t)(lo - abase);
-    meta->nwords = (uint32_t)(hi - lo);
-    meta->staged = staged ? 1u : 0u;
-    meta->lo = lo;
+    const uint64_t abase = lo & ~3ull;
+    const uint32_t words = (uint32_t)(((hi + 3) & ~3ull) - abase);
+    const bool staged = words > 0 && words <= (uint32_t)a.bufw;
+    *meta = SliceMeta{(uint32_t)(lo - abase) | (staged ? 0u : kGlobalSlice), (uint32_t)(hi - lo)};
     if (staged) {
-        mbar_arrive_expect_tx(bar, (uint32_t)bytes);
-        bulk_g2s(buf, a.stream + abase, (uint32_t)bytes, bar);
+        mbar_arrive_expect_tx(bar, words * 4u);
+        bulk_g2s(buf, a.stream + abase, words * 4u, bar);
     } else {
         mbar_arrive(bar);
     }
@@ -257,13 +255,17 @@ __device__ __forceinline__ void payload_event(const Ctx &C, const Src &src, uint
                                               const int lane)
 {
     using Bits = typename T::Bits;
+    // cheap test first: escape entries are the largest entries of a table
+    const uint32_t dmax = max(max(e[0], e[2]), max(e[4], e[6]));
+    const uint32_t vmax = max(max(e[1], e[3]), max(e[5], e[7]));
+    const bool has = act && (dmax >= C.desc_min || vmax >= C.vesc_min);
+    if (!__any_sync(0xFFFFFFFFu, has)) return;
     uint32_t pc = 0;
 #pragma unroll
     for (int p = 0; p < 4; p++)
         pc += (e[2 * p] >= C.desc_min ? 1u : 0u) + (e[2 * p + 1] >= C.vesc_min ? (uint32_t)T::kPayloadWords : 0u);
     if (!act) pc = 0;
     const uint32_t any = __ballot_sync(0xFFFFFFFFu, pc != 0);
-    if (!any) return;
     if (__all_sync(0xFFFFFFFFu, pc <= 1u)) {
         // common case (e.g. one escaped first column per row): every lane
         // reads at most one word, its rank among the escaping lanes
@@ -531,18 +533,15 @@ __global__ void __launch_bounds__(kThreads, 1) dtans_kernel(const KernelArgs a)
         const SliceMeta md = meta[b];
         const uint32_t row = s * kSliceRows + lane;
         const bool inrow = row < rows;
-        if (md.staged) {
+        if (!(md.off & kGlobalSlice)) {
             const SmemSrc src{smem_u32(bufs + b * a.bufw) + md.off * 4u};
             decode_slice<V, kDecode, kHasY>(a, C, x, src, md.nwords, n, row, inrow, lane);
         } else {
-            const GmemSrc src{a.stream + md.lo};
+            const GmemSrc src{a.stream + __ldg(a.directory + s)};
             decode_slice<V, kDecode, kHasY>(a, C, x, src, md.nwords, n, row, inrow, lane);
         }
         __syncwarp();
-        if (lane == 0 && sr < nsl) {
-            fence_proxy_async();
-            stage_slice(a, rlo, rhi, &bars[b], &meta[b], bufs + b * a.bufw);
-        }
+        if (lane == 0 && sr < nsl) stage_slice(a, rlo, rhi, &bars[b], &meta[b], bufs + b * a.bufw);
         if (++b == kRing) {
             b = 0;
             parity ^= 1u;
