@@ -182,8 +182,8 @@ int configure(dtans_dev *h, const TableBlock &tb, const uint64_t *directory)
         max_words = std::max<uint64_t>(max_words, hi - lo);
     }
     const char *env_t = getenv("DTANS_THREADS");
-    h->threads = env_t ? atoi(env_t) : 768;
-    if (h->threads != 1024 && h->threads != 768) h->threads = 768;
+    h->threads = env_t ? atoi(env_t) : 1024;
+    if (h->threads != 1024 && h->threads != 768) h->threads = 1024;
     const int warps = h->threads / 32;
     const int64_t budget =
         ((int64_t)max_optin - (int64_t)off - dev::kOverrunWords * 4) / (warps * dev::kRing * 4);

@@ -460,8 +460,12 @@ __device__ __forceinline__ void decode_slice(const KernelArgs &a, const Ctx &C, 
             }
         }
     }
-    if (lane == 0 && cur != end) atomicOr(a.err, 1u);
-    if (__any_sync(FULL, n > 0 && col > C.cols_m1) && lane == 0) atomicOr(a.err, 2u);
+    // consumption check (container.py:499-500) and column bound, one vote
+    const bool col_bad = n > 0 && col > C.cols_m1;
+    if (__any_sync(FULL, col_bad || cur != end)) {  // rare: report once per slice
+        const uint32_t cb = __ballot_sync(FULL, col_bad);
+        if (lane == 0) atomicOr(a.err, (cur != end ? 1u : 0u) | (cb ? 2u : 0u));
+    }
     if (!kDecode && inrow) {
         const V res = kHasY ? T::add(acc, yv) : acc;
         reinterpret_cast<V *>(a.out)[row] = res;

@@ -1,0 +1,166 @@
+"""Row sharding across GPUs and the iterated SpMV (power iteration).
+
+The data-parallel unit is the 32-row slice: a contiguous slice range of a
+container, with its directory rebased and the same coding tables, is itself
+a valid container whose decode equals the corresponding rows of the whole
+(the reference's decode walks slices independently, container.py:370-521,
+each from directory[s], :174,190).  So a matrix is row-partitioned into
+nnz-balanced slice ranges, one per rank, and each GPU decodes only its shard.
+
+* single SpMV: no collective at all (y stays sharded);
+* power iteration (BASELINE configs[4]): per iteration, local y = A_r x,
+  all-reduce of sum(y^2) (one double), scale, then an all-gather of the
+  y shards into the next x.  torch.distributed (NCCL over NVLink/NVSwitch)
+  carries the collectives; shards are padded to a common length so
+  all_gather_into_tensor moves them in one call, followed by a compaction.
+
+CPU tests exercise this logic with the gloo backend and an injected SpMV
+(the oracle); the product path always calls the CUDA kernel.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import replace
+
+import numpy as np
+
+from .container import SLICE_HEIGHT, CsrDtansContainer
+from .errors import ParameterError
+
+
+def shard_bounds(c: CsrDtansContainer, nshards: int, balance: str = "nnz") -> np.ndarray:
+    """Slice boundaries [0 = b_0 <= b_1 <= ... <= b_n = nslices] splitting the
+    container into ``nshards`` contiguous slice ranges with balanced nnz
+    (``balance="nnz"``, the north star's rule) or balanced stream words
+    (``"words"``, the decode-time driver)."""
+    if nshards < 1:
+        raise ParameterError("nshards must be >= 1")
+    ns = c.nslices
+    if balance == "nnz":
+        rs = np.zeros(ns * SLICE_HEIGHT, dtype=np.int64)
+        rs[: c.rows] = np.asarray(c.row_symbols, dtype=np.int64) // 2
+        per = rs.reshape(ns, SLICE_HEIGHT).sum(axis=1) if ns else np.zeros(0, np.int64)
+        cum = np.concatenate([[0], np.cumsum(per)])
+    elif balance == "words":
+        cum = np.asarray(c.directory, dtype=np.int64)
+    else:
+        raise ParameterError(f"unknown balance {balance!r}")
+    total = cum[-1] if len(cum) else 0
+    b = np.zeros(nshards + 1, dtype=np.int64)
+    for r in range(1, nshards):
+        b[r] = int(np.searchsorted(cum, total * r / nshards, side="left"))
+    b[nshards] = ns
+    b = np.maximum.accumulate(np.clip(b, 0, ns))
+    return b
+
+
+def shard(c: CsrDtansContainer, s_lo: int, s_hi: int) -> CsrDtansContainer:
+    """Sub-container of slices [s_lo, s_hi): rows [32 s_lo, min(32 s_hi, rows)),
+    same tables and parameters, directory rebased to start at 0."""
+    if not (0 <= s_lo <= s_hi <= c.nslices):
+        raise ParameterError("bad slice range")
+    r0 = s_lo * SLICE_HEIGHT
+    r1 = min(s_hi * SLICE_HEIGHT, c.rows)
+    r1 = max(r0, r1)
+    d = np.asarray(c.directory, dtype=np.uint64)
+    w0, w1 = int(d[s_lo]), int(d[s_hi])
+    rs = np.asarray(c.row_symbols[r0:r1], dtype=np.uint32).copy()
+    return replace(
+        c, rows=r1 - r0, nnz=int(rs.astype(np.int64).sum() // 2), row_symbols=rs,
+        directory=(d[s_lo: s_hi + 1] - np.uint64(w0)).astype(np.uint64),
+        stream=np.asarray(c.stream[w0:w1], dtype=np.uint32).copy(), _cache={})
+
+
+def shard_rows(c: CsrDtansContainer, bounds: np.ndarray):
+    """Row ranges [(r0, r1)] of the shards given slice bounds."""
+    return [(int(bounds[i]) * SLICE_HEIGHT, min(int(bounds[i + 1]) * SLICE_HEIGHT, c.rows))
+            for i in range(len(bounds) - 1)]
+
+
+class ShardedSpMV:
+    """One rank's view: its shard on its GPU plus the row layout of all shards.
+
+    ``spmv_fn(x, y_or_None, out)`` computes the local product; by default the
+    CUDA kernel of the shard (``DeviceContainer.spmv``)."""
+
+    def __init__(self, c: CsrDtansContainer, rank: int, world: int, device=None, spmv_fn=None,
+                 balance: str = "nnz", bounds=None):
+        self.bounds = shard_bounds(c, world, balance) if bounds is None else np.asarray(bounds)
+        self.rows_of = shard_rows(c, self.bounds)
+        self.rank, self.world = rank, world
+        self.cols = c.cols
+        self.global_rows = c.rows
+        self.local = shard(c, int(self.bounds[rank]), int(self.bounds[rank + 1]))
+        self.max_rows = max(r1 - r0 for r0, r1 in self.rows_of) if self.rows_of else 0
+        self.device = device
+        if spmv_fn is None:
+            dev = self.local.device(device.index if hasattr(device, "index") and device.index is not None else 0)
+            self._dev = dev
+
+            def spmv_fn(x, y, out):
+                return dev.spmv(x, y, out)
+        self.spmv_fn = spmv_fn
+
+    def spmv(self, x, y=None, out=None):
+        """Local rows of A x (+ y)."""
+        import torch
+        if out is None:
+            out = torch.empty(self.local.rows, dtype=x.dtype, device=x.device)
+        if self.local.rows == 0:
+            return out
+        return self.spmv_fn(x, y, out)
+
+
+def power_iteration(op: ShardedSpMV, x0, iters: int, group=None, return_history: bool = False):
+    """x <- A x / ||A x||_2 for ``iters`` iterations over all ranks.
+
+    x0: full-length vector on this rank's device (every rank holds the same
+    x).  Returns (x, lambda) where lambda = ||A x_{k-1}|| at the last step
+    (the dominant eigenvalue estimate for a Perron matrix)."""
+    import torch
+    import torch.distributed as dist
+    world = op.world
+    if len(x0) != op.cols or op.cols != op.global_rows:
+        raise ParameterError("power iteration needs a square matrix and a full-length x0")
+    x = x0.clone()
+    dtype, device = x.dtype, x.device
+    pad = torch.zeros(op.max_rows, dtype=dtype, device=device)
+    gathered = torch.empty(world * op.max_rows, dtype=dtype, device=device)
+    # compaction index from the padded gather layout to the row order
+    idx = torch.cat([torch.arange(r * op.max_rows, r * op.max_rows + (r1 - r0), device=device)
+                     for r, (r0, r1) in enumerate(op.rows_of)]) if world > 1 else None
+    sq = torch.zeros(1, dtype=torch.float64, device=device)
+    hist = []
+    lam = float("nan")
+    for _ in range(iters):
+        y = pad[: op.local.rows]
+        op.spmv(x, None, y)
+        sq[0] = torch.dot(y.to(torch.float64), y.to(torch.float64))
+        if world > 1:
+            dist.all_reduce(sq, group=group)
+        norm = torch.sqrt(sq)
+        lam = norm
+        if world > 1:
+            dist.all_gather_into_tensor(gathered, pad, group=group)
+            x = torch.index_select(gathered, 0, idx)
+        else:
+            x = y.clone()
+        x.div_(norm.to(dtype))
+        if return_history:
+            hist.append(float(norm.item()))
+    lam = float(lam.item()) if torch.is_tensor(lam) else lam
+    return (x, lam, hist) if return_history else (x, lam)
+
+
+def reference_power_iteration(A_csr, x0: np.ndarray, iters: int):
+    """Plain numpy power iteration on a CSR matrix (test checker)."""
+    import scipy.sparse as sp
+    A = sp.csr_matrix((A_csr.values, A_csr.col_idx, A_csr.row_start), shape=(A_csr.rows, A_csr.cols))
+    x = x0.astype(np.float64).copy()
+    lam = math.nan
+    for _ in range(iters):
+        y = A @ x
+        lam = float(np.sqrt(np.dot(y, y)))
+        x = y / lam
+    return x, lam

@@ -86,3 +86,32 @@ def test_larger_matrices_vs_oracle(gen):
     out = P.spmv(c, x, y)
     ref = O.spmv(O.parse(P.serialize(c)), x, y, threads=8)
     assert G.same_bits_or_nan(out, ref)
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_spmv_on_gpu_equals_full(world):
+    from paper_2603_01915_b200 import distributed as D
+    m = synth.rmat(13, 60000, seed=5)
+    x, y = synth.vectors(m)
+    c = P.encode_matrix(m)
+    full = P.spmv(c, x, y)
+    b = D.shard_bounds(c, world)
+    xt = torch.from_numpy(x).cuda()
+    for i, (r0, r1) in enumerate(D.shard_rows(c, b)):
+        sc = D.shard(c, int(b[i]), int(b[i + 1]))
+        out = sc.device(0).spmv(xt, torch.from_numpy(y[r0:r1]).cuda()) if sc.rows else None
+        if sc.rows:
+            sc.device(0).check()
+            assert G.same_bits_or_nan(out.cpu().numpy(), full[r0:r1])
+
+
+def test_power_iteration_single_gpu():
+    from paper_2603_01915_b200 import distributed as D
+    m = synth.banded(20000, 32, positive=True, seed=3)
+    c = P.encode_matrix(m)
+    op = D.ShardedSpMV(c, 0, 1, device=torch.device("cuda", 0))
+    x0 = torch.full((m.cols,), 1.0 / np.sqrt(m.cols), dtype=torch.float64, device="cuda")
+    x, lam = D.power_iteration(op, x0, 30)
+    xr, lr = D.reference_power_iteration(m, np.full(m.cols, 1.0 / np.sqrt(m.cols)), 30)
+    assert abs(lam - lr) <= 1e-12 * lr
+    assert np.allclose(x.cpu().numpy(), xr, rtol=1e-11, atol=1e-14)
