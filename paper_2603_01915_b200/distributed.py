@@ -102,6 +102,28 @@ class ShardedSpMV:
                 return dev.spmv(x, y, out)
         self.spmv_fn = spmv_fn
 
+    @classmethod
+    def from_local(cls, local: CsrDtansContainer, rows_of, rank: int, world: int, device=None,
+                   spmv_fn=None):
+        """A rank that encoded only its own row block (``local``), given the
+        global row layout ``rows_of`` = [(r0, r1)] of all ranks."""
+        self = cls.__new__(cls)
+        self.rows_of = [(int(a), int(b)) for a, b in rows_of]
+        self.bounds = None
+        self.rank, self.world = rank, world
+        self.cols = local.cols
+        self.global_rows = self.rows_of[-1][1]
+        self.local = local
+        self.max_rows = max(r1 - r0 for r0, r1 in self.rows_of)
+        self.device = device
+        if spmv_fn is None:
+            dev = local.device(device.index if device is not None and device.index is not None else 0)
+
+            def spmv_fn(x, y, out):
+                return dev.spmv(x, y, out)
+        self.spmv_fn = spmv_fn
+        return self
+
     def spmv(self, x, y=None, out=None):
         """Local rows of A x (+ y)."""
         import torch

@@ -76,6 +76,39 @@ def banded(rows: int, band: int = 27, levels: int = 256, seed: int = 0,
     return CsrMatrix(rows, rows, row_start, cols, vals)
 
 
+def _splitmix64(z: np.ndarray) -> np.ndarray:
+    z = (z + np.uint64(0x9E3779B97F4A7C15)).astype(np.uint64)
+    z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+    z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+    return z ^ (z >> np.uint64(31))
+
+
+def banded_rows(rows_total: int, r0: int, r1: int, band: int = 32, levels: int = 256, seed: int = 0,
+                positive: bool = True, dtype=np.float64) -> CsrMatrix:
+    """Rows [r0, r1) of the ``rows_total``-row banded matrix of ``banded``'s
+    shape, values from a counter-based hash of (seed, row, column), so every
+    row block of the same global matrix is generated independently and
+    identically on each rank (power iteration / scaling runs)."""
+    half = band // 2
+    i = np.arange(r0, r1, dtype=np.int64)
+    lo = np.maximum(0, i - half)
+    hi = np.minimum(rows_total, i - half + band)
+    cnt = hi - lo
+    row_start = np.zeros(len(i) + 1, dtype=np.int64)
+    np.cumsum(cnt, out=row_start[1:])
+    nnz = int(row_start[-1])
+    row_of = np.repeat(np.arange(len(i), dtype=np.int64), cnt)
+    cols = lo[row_of] + (np.arange(nnz, dtype=np.int64) - row_start[row_of])
+    key = (i[row_of].astype(np.uint64) * np.uint64(rows_total) + cols.astype(np.uint64)) ^ np.uint64(seed * 0x5851F42D)
+    lvl = (_splitmix64(key) % np.uint64(levels)).astype(np.int64)
+    del key, row_of
+    if positive:
+        alphabet = (np.arange(levels, dtype=np.float64) + 1.0) / levels
+    else:
+        alphabet = np.linspace(-1.0, 1.0, levels)
+    return CsrMatrix(len(i), rows_total, row_start, cols, alphabet.astype(dtype)[lvl])
+
+
 def rmat(scale: int, nnz: int, seed: int = 0, probs=(57, 19, 19, 5),
          dtype=np.float32, batch: int = 1 << 24) -> CsrMatrix:
     """Config 3: R-MAT (a,b,c,d)=(.57,.19,.19,.05) adjacency, edges drawn
