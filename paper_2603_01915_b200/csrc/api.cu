@@ -8,6 +8,7 @@
 #include <cstring>
 #include <vector>
 
+#include "checkpoints.h"
 #include "common.h"
 #include "kernels.cuh"
 
@@ -31,6 +32,10 @@ struct dtans_dev {
     int ctas = 0, threads = 1024, smem = 0;
     int64_t launches = 0;
     int64_t staged_slices = 0;  // slices whose stream fits a ring buffer
+    // long-slice checkpoint index
+    void *d_long = nullptr;     // tasks + pool + slices + partials
+    size_t long_bytes = 0;
+    int task_ctas = 0, task_smem = 0;
 };
 
 namespace {
@@ -163,6 +168,19 @@ int configure(dtans_dev *h, const TableBlock &tb, const uint64_t *directory)
     a.nwords = h->nwords;
     a.err = h->d_err;
     int max_optin = 0, sms = 0;
+    if (a.ntasks) {
+        h->task_smem = (int)align_up((size_t)a.table_bytes, 16);
+        CK(cudaFuncSetAttribute(dev::dtans_task_kernel<V, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                h->task_smem), "cudaFuncSetAttribute");
+        CK(cudaFuncSetAttribute(dev::dtans_task_kernel<V, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                h->task_smem), "cudaFuncSetAttribute");
+        int per = 0, nsm = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, dev::dtans_task_kernel<V, false>, 512, h->task_smem),
+           "occupancy");
+        CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, h->device), "sm count");
+        h->task_ctas = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)nsm * std::max(per, 1),
+                                                                    ((int64_t)a.ntasks + 15) / 16));
+    }
     CK(cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->device), "attr");
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device), "sm count");
     size_t off = (size_t)a.table_bytes;
@@ -232,6 +250,20 @@ int launch(dtans_dev *h, const V *x, const V *y, V *out, const int64_t *row_star
         return 0;
     });
     h->launches++;
+    if (a.ntasks) {
+        if (decode_only) {
+            dev::dtans_task_kernel<V, true><<<h->task_ctas, 512, h->task_smem, st>>>(a);
+            h->launches++;
+        } else {
+            dev::dtans_task_kernel<V, false><<<h->task_ctas, 512, h->task_smem, st>>>(a);
+            const unsigned nb = (a.nlong * 32u + 255u) / 256u;
+            if (y != nullptr)
+                dev::dtans_finalize_kernel<V, true><<<nb, 256, 0, st>>>(a);
+            else
+                dev::dtans_finalize_kernel<V, false><<<nb, 256, 0, st>>>(a);
+            h->launches += 2;
+        }
+    }
     CK(cudaGetLastError(), "kernel launch");
     return DTANS_OK;
 }
@@ -265,6 +297,19 @@ extern "C" int dtans_upload(const dtans_container_view *c, int device, dtans_dev
     h->nwords = c->nwords;
     h->precision = c->precision;
     const TableBlock tb = build_table_block(c->tables, c->precision);
+    LongIndex li;
+    {
+        const char *e1 = getenv("DTANS_LONG_SEG"), *e2 = getenv("DTANS_CHUNK");
+        const int long_seg = e1 ? atoi(e1) : 64, chunk = e2 ? atoi(e2) : 32;
+        const int rc0 = build_long_index(c, long_seg, std::max(1, chunk), li);
+        if (rc0) {
+            delete h;
+            return rc0;
+        }
+        h->base.long_seg = li.tasks.empty() ? 0xFFFFFFFFu : (uint32_t)long_seg;
+        h->base.ntasks = (uint32_t)li.tasks.size();
+        h->base.nlong = (uint32_t)li.slices.size();
+    }
 
     // one allocation: [tables][row_symbols][directory][stream + pad][err]
     size_t off = 0;
@@ -301,10 +346,31 @@ extern "C" int dtans_upload(const dtans_container_view *c, int device, dtans_dev
         if (ce == cudaSuccess) ce = cudaMemset(h->d_err, 0, 16);
         if (ce != cudaSuccess) rc = cuda_fail(ce, "memset");
     }
+    if (rc == DTANS_OK && !li.tasks.empty()) {
+        const size_t tb_b = align_up(li.tasks.size() * sizeof(LongTask), 256);
+        const size_t pl_b = align_up(li.pool.size() * 4, 256);
+        const size_t ls_b = align_up(li.slices.size() * sizeof(LongSlice), 256);
+        const size_t pa_b = align_up((size_t)li.nparts * 32 * c->precision, 256);
+        h->long_bytes = tb_b + pl_b + ls_b + pa_b;
+        cudaError_t ce = cudaMalloc(&h->d_long, h->long_bytes);
+        if (ce != cudaSuccess) {
+            rc = fail(DTANS_E_NOMEM, "cudaMalloc(long index): %s", cudaGetErrorString(ce));
+        } else {
+            char *lb = (char *)h->d_long;
+            h->base.tasks = (const LongTask *)lb;
+            h->base.ck_pool = (const uint32_t *)(lb + tb_b);
+            h->base.longs = (const LongSlice *)(lb + tb_b + pl_b);
+            h->base.partials = lb + tb_b + pl_b + ls_b;
+            cp(lb, li.tasks.data(), li.tasks.size() * sizeof(LongTask));
+            cp(lb + tb_b, li.pool.data(), li.pool.size() * 4);
+            cp(lb + tb_b + pl_b, li.slices.data(), li.slices.size() * sizeof(LongSlice));
+        }
+    }
     if (rc == DTANS_OK)
         rc = c->precision == 8 ? configure<double>(h, tb, c->directory) : configure<float>(h, tb, c->directory);
     if (rc != DTANS_OK) {
         cudaFree(h->d_base);
+        if (h->d_long) cudaFree(h->d_long);
         delete h;
         return rc;
     }
@@ -317,6 +383,7 @@ extern "C" void dtans_free(dtans_dev *h)
     if (!h) return;
     cudaSetDevice(h->device);
     if (h->d_base) cudaFree(h->d_base);
+    if (h->d_long) cudaFree(h->d_long);
     if (h->d_io) cudaFree(h->d_io);
     delete h;
 }
@@ -325,7 +392,7 @@ extern "C" int dtans_info(const dtans_dev *h, int64_t *device_bytes, int32_t *ct
                           int32_t *warps_per_cta, int32_t *smem_bytes)
 {
     if (!h) return fail(DTANS_E_PARAM, "null handle");
-    if (device_bytes) *device_bytes = (int64_t)h->d_bytes;
+    if (device_bytes) *device_bytes = (int64_t)(h->d_bytes + h->long_bytes);
     if (ctas) *ctas = h->ctas;
     if (warps_per_cta) *warps_per_cta = h->threads / 32;
     if (smem_bytes) *smem_bytes = h->smem;

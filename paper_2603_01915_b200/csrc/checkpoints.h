@@ -1,0 +1,34 @@
+// Long-slice checkpoint index shared by the host builder and the kernels.
+#pragma once
+#include <cstdint>
+#include <vector>
+
+#include "../../include/dtans.h"
+
+namespace dtans {
+
+// One warp task: segments [j0, j1) of a long slice.  ck indexes the
+// checkpoint record in the pool ({active lane mask, then per active lane
+// w0, w1, w2, d, r, col}); 0xFFFFFFFF = start from the slice's init events.
+struct LongTask {
+    uint32_t slice, j0, j1, part;  // part: partial-sum slot
+    uint32_t cur0, cur1;           // slice-relative cursor at j0 and expected at j1
+    uint32_t ck, last;             // last: j1 is the slice's final segment count
+};
+
+struct LongSlice {
+    uint32_t slice, part_base, nparts, pad;
+};
+
+struct LongIndex {
+    std::vector<LongTask> tasks;
+    std::vector<uint32_t> pool;
+    std::vector<LongSlice> slices;
+    uint32_t nparts = 0;
+};
+
+// Slices whose longest row has more than seg_threshold segments are split
+// into tasks of `chunk` segments.
+int build_long_index(const dtans_container_view *c, int seg_threshold, int chunk, LongIndex &out);
+
+}  // namespace dtans

@@ -31,6 +31,8 @@
 #pragma once
 #include <cstdint>
 
+#include "checkpoints.h"
+
 namespace dtans {
 namespace dev {
 
@@ -74,6 +76,13 @@ struct KernelArgs {
     int64_t *dec_cols;            // decode kernel only
     void *dec_vals;               // decode kernel only
     unsigned int *err;            // bit 0: consumption mismatch, bit 1: column OOB
+    // long slices (checkpoint index, checkpoints.cpp)
+    uint32_t long_seg;            // slices with more segments go to the task kernel
+    uint32_t ntasks, nlong;
+    const LongTask *tasks;
+    const uint32_t *ck_pool;
+    const LongSlice *longs;
+    void *partials;               // V[nparts][32]
 };
 
 __device__ __forceinline__ uint32_t lanemask_lt()
@@ -325,53 +334,64 @@ __device__ __forceinline__ void group(uint32_t m0, uint32_t m1, uint32_t m2, uin
     dg = D * q3 + (D + (m3 & 0xFFu));
 }
 
-template <typename V, bool kDecode, bool kHasY, class Src>
-__device__ __forceinline__ void decode_slice(const KernelArgs &a, const Ctx &C, const V *__restrict__ x,
-                                             const Src src, const uint32_t end, const uint32_t n,
-                                             const uint32_t row, const bool inrow, const int lane)
+// 32x32 -> 64 multiply-add returning the two halves (forces 32-bit compares
+// on the high word instead of a 64-bit compare).
+__device__ __forceinline__ void mad_wide(uint32_t a, uint32_t b, uint32_t c_lo, uint32_t c_hi, uint32_t &lo,
+                                         uint32_t &hi)
+{
+    asm("{\n.reg .u64 t, c;\n"
+        "mov.b64 c, {%2, %3};\n"
+        "mad.wide.u32 t, %4, %5, c;\n"
+        "mov.b64 {%0, %1}, t;\n}"
+        : "=r"(lo), "=r"(hi)
+        : "r"(c_lo), "r"(c_hi), "r"(a), "r"(b));
+}
+
+// d*B + D with B-1 = bm1 (< 2^32), d < 2^32, D < 2^32: d*bm1 + (d + D).
+__device__ __forceinline__ void fold(uint32_t d, uint32_t bm1, uint32_t D, uint32_t &lo, uint32_t &hi)
+{
+    uint32_t s_lo, s_hi;
+    asm("add.cc.u32 %0, %2, %3;\naddc.u32 %1, 0, 0;" : "=r"(s_lo), "=r"(s_hi) : "r"(d), "r"(D));
+    mad_wide(d, bm1, s_lo, s_hi, lo, hi);
+}
+
+// One segment that is not the final one of the slice (some lane folds
+// digits).  kHot: every lane is active and not in its last segment (all
+// 4 pairs valid, all lanes load/extract), so the per-lane predicates vanish.
+template <typename V, bool kDecode, bool kHot, class Src>
+__device__ __forceinline__ void full_segment(const KernelArgs &a, const Ctx &C, const V *__restrict__ x,
+                                             const Src &src, const uint32_t j, const uint32_t n,
+                                             const uint32_t nseg, uint32_t &w0, uint32_t &w1, uint32_t &w2,
+                                             uint32_t &d, uint32_t &r, uint32_t &cur, uint32_t &col, V &acc,
+                                             int64_t &out_pos, const int lane)
 {
     using T = ValueTraits<V>;
     using Bits = typename T::Bits;
     const uint32_t FULL = 0xFFFFFFFFu;
-    const uint32_t nseg = (n + 7u) >> 3;
-    const uint32_t maxn = __reduce_max_sync(FULL, n);
-    const uint32_t max_nseg = (maxn + 7u) >> 3;
-    V yv = V(0);
-    if (kHasY) yv = __ldg(reinterpret_cast<const V *>(a.y) + (inrow ? row : 0u));
-    int64_t out_pos = 0;
-    if (kDecode && inrow) out_pos = __ldg(a.row_start + row);
-
-    // init events (container.py:426-429): 3 words per active lane
-    uint32_t w0 = 0, w1 = 0, w2 = 0, cur;
-    {
-        const uint32_t am = __ballot_sync(FULL, n > 0);
-        const uint32_t cnt = __popc(am), rk = __popc(am & C.lt);
-        if (n > 0) {
-            w0 = src(rk);
-            w1 = src(cnt + rk);
-            w2 = src(2 * cnt + rk);
-        }
-        cur = 3 * cnt;
-    }
-    uint32_t d = 0, r = 1, col = 0;
-    V acc = V(0);
-    bool bad = false;
-
-    // Segments where some lane still folds digits: all 8 slots, radix chain.
-    for (uint32_t j = 0; j + 1 < max_nseg; j++) {  // (max_nseg == 0: no iterations)
-        const bool act = j < nseg;
-        const bool notlast = j + 1 < nseg;
-        uint32_t so[8], e[8], ds[4];
-        Bits vs[4];
-        slot_offsets(w0, w1, w2, so);
+    const bool act = kHot || j < nseg;
+    const bool notlast = kHot || j + 1 < nseg;
+    uint32_t so[8], e[8], ds[4];
+    Bits vs[4];
+    slot_offsets(w0, w1, w2, so);
 #pragma unroll
-        for (int p = 0; p < 4; p++) lookup_pair<Bits>(C, so[2 * p], so[2 * p + 1], e[2 * p], e[2 * p + 1], ds[p], vs[p]);
-        payload_event<T>(C, src, cur, act, e, ds, vs, lane);
-        V xv[4];
+    for (int p = 0; p < 4; p++) lookup_pair<Bits>(C, so[2 * p], so[2 * p + 1], e[2 * p], e[2 * p + 1], ds[p], vs[p]);
+    payload_event<T>(C, src, cur, act, e, ds, vs, lane);
+    V xv[4];
 #pragma unroll
-        for (int p = 0; p < 4; p++) {
+    for (int p = 0; p < 4; p++) {
+        const bool valid = kHot || 8u * j + 2u * p < n;
+        if (kHot) {
+            col += ds[p];
+            if (kDecode) {
+                a.dec_cols[out_pos] = (int64_t)col;
+                reinterpret_cast<Bits *>(a.dec_vals)[out_pos] = vs[p];
+                out_pos++;
+            } else {
+                xv[p] = __ldg(x + min(col, C.cols_m1));
+            }
+        } else {
             xv[p] = V(0);
-            if (8u * j + 2u * p < n) {
+            if (valid) {
                 col += ds[p];
                 if (kDecode) {
                     a.dec_cols[out_pos] = (int64_t)col;
@@ -382,56 +402,96 @@ __device__ __forceinline__ void decode_slice(const KernelArgs &a, const Ctx &C, 
                 }
             }
         }
-        // mixed-radix checks (container.py:478-497): bases decide load vs extract
-        uint32_t bm1a, dga, bm1b, dgb;
-        group(e[0], e[1], e[2], e[3], bm1a, dga);
-        group(e[4], e[5], e[6], e[7], bm1b, dgb);
-        const unsigned long long r1 = (unsigned long long)r * bm1a + r;
-        const uint32_t r1h = (uint32_t)(r1 >> 32);
-        const bool ext0 = r1h != 0u;
-        const uint32_t ra = ext0 ? r1h : (uint32_t)r1;
-        const unsigned long long r2 = (unsigned long long)ra * bm1b + ra;
-        const uint32_t r2h = (uint32_t)(r2 >> 32);
-        const bool ext1 = r2h != 0u;
-        const uint32_t m_ld0 = __ballot_sync(FULL, notlast && !ext0);
-        const uint32_t m_ld1 = __ballot_sync(FULL, notlast && !ext1);
-        const uint32_t m_nl = __ballot_sync(FULL, notlast);
-        const uint32_t c1 = cur + __popc(m_ld0);
-        const uint32_t c2 = c1 + __popc(m_ld1);
-        const uint32_t lw0 = src(cur + __popc(m_ld0 & C.lt));
-        const uint32_t lw1 = src(c1 + __popc(m_ld1 & C.lt));
-        const uint32_t lw2 = src(c2 + __popc(m_nl & C.lt));
-        cur = c2 + __popc(m_nl);
-        if (notlast) {
-            const unsigned long long d1 = (unsigned long long)d * bm1a + ((unsigned long long)d + dga);
-            const uint32_t da = ext0 ? (uint32_t)(d1 >> 32) : (uint32_t)d1;
-            w0 = ext0 ? (uint32_t)d1 : lw0;
-            const unsigned long long d2 = (unsigned long long)da * bm1b + ((unsigned long long)da + dgb);
-            w1 = ext1 ? (uint32_t)d2 : lw1;
-            d = ext1 ? (uint32_t)(d2 >> 32) : (uint32_t)d2;
-            r = ext1 ? r2h : (uint32_t)r2;
-            w2 = lw2;
-        }
-        if (!kDecode) {
+    }
+    // mixed-radix checks (container.py:478-497): bases decide load vs extract
+    uint32_t bm1a, dga, bm1b, dgb;
+    group(e[0], e[1], e[2], e[3], bm1a, dga);
+    group(e[4], e[5], e[6], e[7], bm1b, dgb);
+    uint32_t r1l, r1h, r2l, r2h;
+    mad_wide(r, bm1a, r, 0u, r1l, r1h);
+    const bool ext0 = r1h != 0u;
+    const uint32_t ra = ext0 ? r1h : r1l;
+    mad_wide(ra, bm1b, ra, 0u, r2l, r2h);
+    const bool ext1 = r2h != 0u;
+    const uint32_t m_ld0 = __ballot_sync(FULL, notlast && !ext0);
+    const uint32_t m_ld1 = __ballot_sync(FULL, notlast && !ext1);
+    const uint32_t m_nl = kHot ? FULL : __ballot_sync(FULL, notlast);
+    const uint32_t c1 = cur + __popc(m_ld0);
+    const uint32_t c2 = c1 + __popc(m_ld1);
+    const uint32_t lw0 = src(cur + __popc(m_ld0 & C.lt));
+    const uint32_t lw1 = src(c1 + __popc(m_ld1 & C.lt));
+    const uint32_t lw2 = src(c2 + (kHot ? (uint32_t)lane : __popc(m_nl & C.lt)));
+    cur = c2 + (kHot ? 32u : __popc(m_nl));
+    if (notlast) {
+        uint32_t d1l, d1h, d2l, d2h;
+        fold(d, bm1a, dga, d1l, d1h);
+        const uint32_t da = ext0 ? d1h : d1l;
+        w0 = ext0 ? d1l : lw0;
+        fold(da, bm1b, dgb, d2l, d2h);
+        w1 = ext1 ? d2l : lw1;
+        d = ext1 ? d2h : d2l;
+        r = ext1 ? r2h : r2l;
+        w2 = lw2;
+    }
+    if (!kDecode) {
 #pragma unroll
-            for (int p = 0; p < 4; p++)
-                if (8u * j + 2u * p < n) acc = T::add(acc, T::mul(T::from_bits(vs[p]), xv[p]));
-        }
-        if (cur > end) {  // uniform: corrupt slice, stop before reading further
-            bad = true;
-            break;
+        for (int p = 0; p < 4; p++) {
+            if (kHot) {
+                acc = T::add(acc, T::mul(T::from_bits(vs[p]), xv[p]));
+            } else if (8u * j + 2u * p < n) {
+                acc = T::add(acc, T::mul(T::from_bits(vs[p]), xv[p]));
+            }
         }
     }
-    // Final segment: every active lane is in its last segment, so no digits
-    // are folded and no checks/unconditional loads happen; pairs past the
-    // longest row are skipped (pads need lookups only when they may escape).
-    if (max_nseg > 0 && !bad) {
-        const uint32_t j = max_nseg - 1;
-        const bool act = j < nseg;
+}
+
+// Per-lane decoder state carried between segments (and restored from a
+// long-slice checkpoint).
+template <typename V> struct LaneState {
+    uint32_t w0, w1, w2, d, r, col, cur;
+    V acc;
+    int64_t out_pos;
+};
+
+// Segments [j0, j1) of a slice (j1 <= max_nseg).  If j1 == max_nseg the
+// last one is the final segment: every active lane is in its last segment,
+// so no digits are folded and no checks/unconditional loads happen, and
+// pairs past the longest row are skipped (pads need lookups only when they
+// may escape).  Returns false if the cursor ran past `end` (corrupt slice).
+template <typename V, bool kDecode, class Src>
+__device__ __forceinline__ bool decode_range(const KernelArgs &a, const Ctx &C, const V *__restrict__ x,
+                                             const Src &src, const uint32_t end, const uint32_t n,
+                                             const uint32_t maxn, const uint32_t j0, const uint32_t j1,
+                                             LaneState<V> &st, const int lane)
+{
+    using T = ValueTraits<V>;
+    using Bits = typename T::Bits;
+    const uint32_t FULL = 0xFFFFFFFFu;
+    const uint32_t nseg = (n + 7u) >> 3;
+    const uint32_t max_nseg = (maxn + 7u) >> 3;
+    const uint32_t min_nseg = __reduce_min_sync(FULL, nseg);
+    const uint32_t jfull = min(j1, max_nseg - 1u);  // segments that fold digits: [j0, jfull)
+    // segments where every lane is active and folds digits, then segments
+    // where some lane does (per-lane predicates)
+    uint32_t j = j0;
+    const uint32_t jhot = min(jfull, min_nseg > 0 ? min_nseg - 1u : 0u);
+    for (; j < jhot; j++) {
+        full_segment<V, kDecode, true>(a, C, x, src, j, n, nseg, st.w0, st.w1, st.w2, st.d, st.r, st.cur, st.col,
+                                       st.acc, st.out_pos, lane);
+        if (st.cur > end) return false;  // uniform
+    }
+    for (; j < jfull; j++) {
+        full_segment<V, kDecode, false>(a, C, x, src, j, n, nseg, st.w0, st.w1, st.w2, st.d, st.r, st.cur,
+                                        st.col, st.acc, st.out_pos, lane);
+        if (st.cur > end) return false;
+    }
+    if (j1 == max_nseg && max_nseg > 0) {
+        const uint32_t jf = max_nseg - 1;
+        const bool act = jf < nseg;
         uint32_t so[8], e[8], ds[4];
         Bits vs[4];
-        slot_offsets(w0, w1, w2, so);
-        const uint32_t base = 8u * j;
+        slot_offsets(st.w0, st.w1, st.w2, so);
+        const uint32_t base = 8u * jf;
 #pragma unroll
         for (int p = 0; p < 4; p++) {
             if (!C.pads_ok || base + 2u * p < maxn) {  // uniform
@@ -442,34 +502,160 @@ __device__ __forceinline__ void decode_slice(const KernelArgs &a, const Ctx &C, 
                 vs[p] = 0;
             }
         }
-        payload_event<T>(C, src, cur, act, e, ds, vs, lane);
+        payload_event<T>(C, src, st.cur, act, e, ds, vs, lane);
 #pragma unroll
         for (int p = 0; p < 4; p++) {
             if (base + 2u * p < maxn) {  // uniform
                 if (base + 2u * p < n) {
-                    col += ds[p];
+                    st.col += ds[p];
                     if (kDecode) {
-                        a.dec_cols[out_pos] = (int64_t)col;
-                        reinterpret_cast<Bits *>(a.dec_vals)[out_pos] = vs[p];
-                        out_pos++;
+                        a.dec_cols[st.out_pos] = (int64_t)st.col;
+                        reinterpret_cast<Bits *>(a.dec_vals)[st.out_pos] = vs[p];
+                        st.out_pos++;
                     } else {
-                        const V xv = __ldg(x + min(col, C.cols_m1));
-                        acc = T::add(acc, T::mul(T::from_bits(vs[p]), xv));
+                        const V xv = __ldg(x + min(st.col, C.cols_m1));
+                        st.acc = T::add(st.acc, T::mul(T::from_bits(vs[p]), xv));
                     }
                 }
             }
         }
     }
-    // consumption check (container.py:499-500) and column bound, one vote
-    const bool col_bad = n > 0 && col > C.cols_m1;
-    if (__any_sync(FULL, col_bad || cur != end)) {  // rare: report once per slice
-        const uint32_t cb = __ballot_sync(FULL, col_bad);
-        if (lane == 0) atomicOr(a.err, (cur != end ? 1u : 0u) | (cb ? 2u : 0u));
+    return true;
+}
+
+// init events (container.py:426-429): 3 words per active lane
+template <typename V, class Src>
+__device__ __forceinline__ void init_state(const Ctx &C, const Src &src, const uint32_t n, LaneState<V> &st)
+{
+    const uint32_t am = __ballot_sync(0xFFFFFFFFu, n > 0);
+    const uint32_t cnt = __popc(am), rk = __popc(am & C.lt);
+    st.w0 = st.w1 = st.w2 = 0;
+    if (n > 0) {
+        st.w0 = src(rk);
+        st.w1 = src(cnt + rk);
+        st.w2 = src(2 * cnt + rk);
     }
+    st.cur = 3 * cnt;
+    st.d = 0;
+    st.r = 1;
+    st.col = 0;
+    st.acc = V(0);
+}
+
+// consumption check (container.py:499-500) and column bound, one vote
+__device__ __forceinline__ void report(const KernelArgs &a, const Ctx &C, bool ok, uint32_t cur, uint32_t end,
+                                       uint32_t n, uint32_t col, int lane)
+{
+    const bool col_bad = n > 0 && col > C.cols_m1;
+    const bool cur_bad = !ok || cur != end;
+    if (__any_sync(0xFFFFFFFFu, col_bad || cur_bad)) {  // rare: report once per slice
+        const uint32_t cb = __ballot_sync(0xFFFFFFFFu, col_bad);
+        if (lane == 0) atomicOr(a.err, (cur_bad ? 1u : 0u) | (cb ? 2u : 0u));
+    }
+}
+
+template <typename V, bool kDecode, bool kHasY, class Src>
+__device__ __forceinline__ void decode_slice(const KernelArgs &a, const Ctx &C, const V *__restrict__ x,
+                                             const Src src, const uint32_t end, const uint32_t n,
+                                             const uint32_t row, const bool inrow, const int lane)
+{
+    using T = ValueTraits<V>;
+    const uint32_t maxn = __reduce_max_sync(0xFFFFFFFFu, n);
+    const uint32_t max_nseg = (maxn + 7u) >> 3;
+    if (max_nseg > a.long_seg) return;  // long slice: decoded by the task kernel (uniform)
+    V yv = V(0);
+    if (kHasY) yv = __ldg(reinterpret_cast<const V *>(a.y) + (inrow ? row : 0u));
+    LaneState<V> st;
+    st.out_pos = 0;
+    if (kDecode && inrow) st.out_pos = __ldg(a.row_start + row);
+    init_state<V>(C, src, n, st);
+    const bool ok = decode_range<V, kDecode>(a, C, x, src, end, n, maxn, 0u, max_nseg, st, lane);
+    report(a, C, ok, st.cur, end, n, st.col, lane);
     if (!kDecode && inrow) {
-        const V res = kHasY ? T::add(acc, yv) : acc;
+        const V res = kHasY ? T::add(st.acc, yv) : st.acc;
         reinterpret_cast<V *>(a.out)[row] = res;
     }
+}
+
+// Long-slice tasks: each warp decodes segments [j0, j1) of one slice from a
+// checkpoint (or the init events), reading the stream from global memory,
+// and writes its 32 per-lane partial sums (or, when decoding, the columns
+// and value bits of those segments directly).
+template <typename V, bool kDecode>
+__global__ void __launch_bounds__(512, 1) dtans_task_kernel(const KernelArgs a)
+{
+    using Bits = typename ValueTraits<V>::Bits;
+    extern __shared__ __align__(128) unsigned char smem[];
+    {
+        const int4 *srcv = reinterpret_cast<const int4 *>(a.tables);
+        int4 *dst = reinterpret_cast<int4 *>(smem);
+        for (int i = threadIdx.x; i < a.table_bytes / 16; i += blockDim.x) dst[i] = __ldg(srcv + i);
+    }
+    __syncthreads();
+    const uint32_t sbase = smem_u32(smem);
+    Ctx C;
+    C.dtab = sbase;
+    C.vtab = sbase + kSlots * 4;
+    C.ddict = sbase + (uint32_t)a.off_ddict;
+    C.vdict = sbase + (uint32_t)a.off_vdict;
+    C.desc_min = a.desc_min;
+    C.vesc_min = a.vesc_min;
+    C.cols_m1 = (uint32_t)(a.cols - 1);
+    C.lt = lanemask_lt();
+    C.pads_ok = a.pads_ok != 0;
+    const V *__restrict__ x = reinterpret_cast<const V *>(a.x);
+    const int lane = threadIdx.x & 31;
+    const uint32_t warps = blockDim.x >> 5;
+    for (uint32_t t = blockIdx.x * warps + (threadIdx.x >> 5); t < a.ntasks; t += gridDim.x * warps) {
+        const LongTask tk = a.tasks[t];
+        const uint32_t row = tk.slice * kSliceRows + lane;
+        const bool inrow = row < (uint32_t)a.rows;
+        const uint32_t n = inrow ? __ldg(a.row_symbols + row) : 0u;
+        const uint32_t maxn = __reduce_max_sync(0xFFFFFFFFu, n);
+        const uint64_t lo = __ldg(a.directory + tk.slice);
+        const uint32_t end = (uint32_t)(__ldg(a.directory + tk.slice + 1) - lo);
+        const GmemSrc src{a.stream + lo};
+        LaneState<V> st;
+        st.out_pos = 0;
+        if (tk.ck == 0xFFFFFFFFu) {
+            init_state<V>(C, src, n, st);
+        } else {
+            const uint32_t mask = __ldg(a.ck_pool + tk.ck);
+            const bool active = (mask >> lane) & 1u;
+            const uint32_t *p = a.ck_pool + tk.ck + 1 + 6 * __popc(mask & C.lt);
+            st.w0 = active ? __ldg(p + 0) : 0u;
+            st.w1 = active ? __ldg(p + 1) : 0u;
+            st.w2 = active ? __ldg(p + 2) : 0u;
+            st.d = active ? __ldg(p + 3) : 0u;
+            st.r = active ? __ldg(p + 4) : 1u;
+            st.col = active ? __ldg(p + 5) : 0u;
+            st.cur = tk.cur0;
+            st.acc = V(0);
+        }
+        // decoding: every segment before j0 of an active lane was full (4 pairs)
+        if (kDecode && inrow) st.out_pos = __ldg(a.row_start + row) + 4ll * tk.j0;
+        const bool ok = decode_range<V, kDecode>(a, C, x, src, tk.cur1, n, maxn, tk.j0, tk.j1, st, lane);
+        report(a, C, ok, st.cur, tk.cur1, tk.last ? n : 0u, st.col, lane);
+        if (!kDecode) reinterpret_cast<V *>(a.partials)[(size_t)tk.part * 32 + lane] = st.acc;
+    }
+}
+
+// Long-slice rows: y' = ((p_0 + p_1) + ... + p_k) + y, partials in task order.
+template <typename V, bool kHasY>
+__global__ void dtans_finalize_kernel(const KernelArgs a)
+{
+    using T = ValueTraits<V>;
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= a.nlong * 32u) return;
+    const LongSlice ls = a.longs[i >> 5];
+    const uint32_t lane = i & 31u;
+    const uint32_t row = ls.slice * kSliceRows + lane;
+    if (row >= (uint32_t)a.rows) return;
+    const V *part = reinterpret_cast<const V *>(a.partials);
+    V acc = part[(size_t)ls.part_base * 32 + lane];
+    for (uint32_t k = 1; k < ls.nparts; k++) acc = T::add(acc, part[(size_t)(ls.part_base + k) * 32 + lane]);
+    if (kHasY) acc = T::add(acc, reinterpret_cast<const V *>(a.y)[row]);
+    reinterpret_cast<V *>(a.out)[row] = acc;
 }
 
 // Persistent kernel, one CTA of 32 warps per SM: tables -> shared memory once,

@@ -46,3 +46,42 @@ def same_bits_or_nan(a, b):
     eq = a.view(ui) == b.view(ui)
     both_nan = np.isnan(a) & np.isnan(b)
     return bool(np.all(eq | both_nan))
+
+
+LONG_SEG = 64  # slices whose longest row has more segments use the task kernel
+
+
+def long_slice_rows(row_start, rows):
+    """Boolean mask of rows that live in long slices (decoded as checkpointed
+    tasks, so their reduction order differs from the reference's)."""
+    nnz_row = np.diff(np.asarray(row_start, dtype=np.int64))
+    nseg = (2 * nnz_row + 7) // 8
+    ns = -(-rows // 32)
+    pad = np.zeros(ns * 32, dtype=np.int64)
+    pad[:rows] = nseg
+    long_slice = pad.reshape(ns, 32).max(axis=1) > LONG_SEG
+    return np.repeat(long_slice, 32)[:rows]
+
+
+def check_spmv(out, ref, m, x, y):
+    """Parity policy (north star / SURVEY 8c): bitwise for rows decoded in
+    lockstep order; for long-slice rows |out-ref| <= tol*(sum|a x| + |y|),
+    tol 1e-12 (f64) / 1e-5 (f32); NaN == NaN."""
+    out = np.asarray(out)
+    ref = np.asarray(ref)
+    if out.shape != ref.shape or out.dtype != ref.dtype:
+        return False
+    lr = long_slice_rows(m.row_start, m.rows)
+    if not same_bits_or_nan(out[~lr], ref[~lr]):
+        return False
+    if not lr.any():
+        return True
+    tol = 1e-12 if out.dtype == np.float64 else 1e-5
+    vals = np.abs(np.asarray(m.values, dtype=np.float64))
+    ax = vals * np.abs(np.asarray(x, dtype=np.float64))[np.asarray(m.col_idx)]
+    rows_of = np.repeat(np.arange(m.rows), np.diff(np.asarray(m.row_start)))
+    s = np.bincount(rows_of, weights=ax, minlength=m.rows) + np.abs(np.asarray(y, dtype=np.float64))
+    o, r = out[lr].astype(np.float64), ref[lr].astype(np.float64)
+    both_nan = np.isnan(o) & np.isnan(r)
+    ok = (np.abs(o - r) <= tol * s[lr]) | both_nan | (o == r)
+    return bool(np.all(ok))
