@@ -285,6 +285,8 @@ def main():
     ap.add_argument("--scale", type=float, default=1.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-cusparse", action="store_true")
+    ap.add_argument("--reorder", action="store_true",
+                    help="encode the rows sorted by length (skew toolkit); results in original order")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
 
@@ -314,7 +316,17 @@ def main():
     m, cfg = build_matrix(args.config, args.scale, world, rank)
     t_gen = time.time() - t0
     t0 = time.time()
-    c = P.encode_matrix(m)
+    if args.reorder:
+        # optional row reordering for skewed matrices (sort_rows_by_length):
+        # encodes P*A, the kernel writes y' back in the original row order
+        pm, perm = P.sort_rows_by_length(m)
+        c = P.encode_matrix(pm)
+        c.row_map = perm
+        del pm
+        cfg["row_order"] = "sorted by length (P*A, row_map)"
+    else:
+        c = P.encode_matrix(m)
+        cfg["row_order"] = "natural"
     t_enc = time.time() - t0
     x, y = synth.vectors(m)
     V = np.float64 if c.precision == 8 else np.float32
@@ -431,7 +443,7 @@ def main():
     comp = min(format_size_bytes(m, f, esz) for f in ("csr", "coo", "sell")) / size
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.reorder:
         cpu = cpu_baseline(c, x, y)
 
     info = dc.info()

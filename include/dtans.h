@@ -141,6 +141,14 @@ int dtans_decode(dtans_dev *h, const int64_t *row_start, int64_t *cols,
  * kernels (consumption mismatch / out-of-range column) -> DTANS_E_CORRUPT. */
 int dtans_check(dtans_dev *h, void *stream);
 
+/* Optional output row map for a row-reordered container (the encoding of
+ * P*A produced by sort_rows_by_length): encoded row i is original row
+ * host_map[i], so y is read and y' written at host_map[i] inside the fused
+ * kernel.  host_map must be a permutation of [0, rows); NULL clears it.  An
+ * extension; the container bytes stay the reference's
+ * encoding of P*A. */
+int dtans_set_row_map(dtans_dev *h, const uint32_t *host_map);
+
 /* Number of dtANS kernels launched by this handle so far (bench evidence). */
 int64_t dtans_launch_count(const dtans_dev *h);
 

@@ -99,6 +99,10 @@ class CsrDtansContainer:
     directory: np.ndarray    # uint64 [nslices + 1]
     stream: np.ndarray       # uint32 [words]
     table_records: np.ndarray = field(default=None, repr=False)  # K slot records
+    # optional extension, not serialized: this container encodes P*A and
+    # row_map[i] is the original row of encoded row i (sort_rows_by_length);
+    # spmv then reads y / writes y' in the original order
+    row_map: np.ndarray = field(default=None, repr=False)
     _cache: dict = field(default_factory=dict, repr=False)
 
     @property
@@ -234,11 +238,16 @@ class DeviceContainer:
         _native.check(L.dtans_upload(ctypes.byref(view), int(device), ctypes.byref(h)))
         self._keep = None
         self.handle = h
+        self._fin = weakref.finalize(self, L.dtans_free, h)
+        if c.row_map is not None:
+            rm = np.ascontiguousarray(c.row_map, dtype=np.uint32)
+            if len(rm) != c.rows:
+                raise ParameterError("row_map must have one entry per row")
+            _native.check(L.dtans_set_row_map(h, rm.ctypes.data))
         self.device = int(device)
         self.rows, self.cols, self.nnz, self.precision = c.rows, c.cols, c.nnz, c.precision
         self.row_symbols = c.row_symbols
         self.closed = False
-        self._fin = weakref.finalize(self, L.dtans_free, h)
 
     @property
     def dtype(self):

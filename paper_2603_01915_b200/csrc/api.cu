@@ -35,7 +35,10 @@ struct dtans_dev {
     // long-slice checkpoint index
     void *d_long = nullptr;     // tasks + pool + slices + partials
     size_t long_bytes = 0;
-    int task_ctas = 0, task_smem = 0;
+    int task_ctas = 0, task_smem = 0, solo_ctas = 0;
+    uint32_t *d_row_map = nullptr;  // optional output row map (reordered P*A)
+    uint32_t *d_order = nullptr;    // optional longest-first slice order (dynamic scheduling)
+    uint64_t long_words = ~0ull;    // slices with a larger aligned window are task-decoded
 };
 
 namespace {
@@ -136,16 +139,13 @@ TableBlock build_table_block(const uint8_t *recs, int precision)
 
 // Dispatch on the compile-time CTA size.
 template <typename V, class F>
-int with_kernel(int threads, F &&f)
+int with_kernel(bool dyn, F &&f)
 {
-    switch (threads) {
-    case 768:
-        return f(dev::dtans_kernel<V, false, true, 768>, dev::dtans_kernel<V, false, false, 768>,
-                 dev::dtans_kernel<V, true, false, 768>);
-    default:
-        return f(dev::dtans_kernel<V, false, true, 1024>, dev::dtans_kernel<V, false, false, 1024>,
-                 dev::dtans_kernel<V, true, false, 1024>);
-    }
+    if (dyn)
+        return f(dev::dtans_kernel<V, false, true, true, 1024>, dev::dtans_kernel<V, false, false, true, 1024>,
+                 dev::dtans_kernel<V, true, false, true, 1024>);
+    return f(dev::dtans_kernel<V, false, true, false, 1024>, dev::dtans_kernel<V, false, false, false, 1024>,
+             dev::dtans_kernel<V, true, false, false, 1024>);
 }
 
 template <typename V>
@@ -167,9 +167,14 @@ int configure(dtans_dev *h, const TableBlock &tb, const uint64_t *directory)
     a.nslices = h->nslices;
     a.nwords = h->nwords;
     a.err = h->d_err;
+    a.work_counter = h->d_err + 8;
     int max_optin = 0, sms = 0;
-    if (a.ntasks) {
+    if (a.nlong) {
         h->task_smem = (int)align_up((size_t)a.table_bytes, 16);
+        CK(cudaFuncSetAttribute(dev::dtans_solo_kernel<V, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                h->task_smem), "cudaFuncSetAttribute");
+        CK(cudaFuncSetAttribute(dev::dtans_solo_kernel<V, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                h->task_smem), "cudaFuncSetAttribute");
         CK(cudaFuncSetAttribute(dev::dtans_task_kernel<V, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 h->task_smem), "cudaFuncSetAttribute");
         CK(cudaFuncSetAttribute(dev::dtans_task_kernel<V, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -180,6 +185,11 @@ int configure(dtans_dev *h, const TableBlock &tb, const uint64_t *directory)
         CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, h->device), "sm count");
         h->task_ctas = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)nsm * std::max(per, 1),
                                                                     ((int64_t)a.ntasks + 15) / 16));
+        int pers = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pers, dev::dtans_solo_kernel<V, false>, 256, h->task_smem),
+           "occupancy");
+        h->solo_ctas = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)nsm * std::max(pers, 1),
+                                                                    ((int64_t)a.nsolo + 255) / 256));
     }
     CK(cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->device), "attr");
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device), "sm count");
@@ -197,11 +207,9 @@ int configure(dtans_dev *h, const TableBlock &tb, const uint64_t *directory)
     uint64_t max_words = 4;
     for (int64_t s = 0; s < h->nslices; s++) {
         const uint64_t lo = directory[s] & ~3ull, hi = (directory[s + 1] + 3) & ~3ull;
-        max_words = std::max<uint64_t>(max_words, hi - lo);
+        if (hi - lo <= h->long_words) max_words = std::max<uint64_t>(max_words, hi - lo);
     }
-    const char *env_t = getenv("DTANS_THREADS");
-    h->threads = env_t ? atoi(env_t) : 1024;
-    if (h->threads != 1024 && h->threads != 768) h->threads = 1024;
+    h->threads = 1024;
     const int warps = h->threads / 32;
     const int64_t budget =
         ((int64_t)max_optin - (int64_t)off - dev::kOverrunWords * 4) / (warps * dev::kRing * 4);
@@ -214,7 +222,7 @@ int configure(dtans_dev *h, const TableBlock &tb, const uint64_t *directory)
     }
     h->smem = (int)(off + ((size_t)warps * dev::kRing * a.bufw + dev::kOverrunWords) * 4);
     int per_sm = 0;
-    int rc = with_kernel<V>(h->threads, [&](auto kspmv, auto kspmv0, auto kdec) -> int {
+    int rc = with_kernel<V>(h->base.dynamic != 0, [&](auto kspmv, auto kspmv0, auto kdec) -> int {
         CK(cudaFuncSetAttribute(kspmv, cudaFuncAttributeMaxDynamicSharedMemorySize, h->smem), "cudaFuncSetAttribute");
         CK(cudaFuncSetAttribute(kspmv0, cudaFuncAttributeMaxDynamicSharedMemorySize, h->smem), "cudaFuncSetAttribute");
         CK(cudaFuncSetAttribute(kdec, cudaFuncAttributeMaxDynamicSharedMemorySize, h->smem), "cudaFuncSetAttribute");
@@ -234,13 +242,14 @@ int launch(dtans_dev *h, const V *x, const V *y, V *out, const int64_t *row_star
 {
     if (h->nslices == 0) return DTANS_OK;
     dev::KernelArgs a = h->base;
+    if (a.dynamic) CK(cudaMemsetAsync(a.work_counter, 0, sizeof(uint32_t), st), "reset work counter");
     a.x = x;
     a.y = y;
     a.out = out;
     a.row_start = row_start;
     a.dec_cols = cols;
     a.dec_vals = vals;
-    with_kernel<V>(h->threads, [&](auto kspmv, auto kspmv0, auto kdec) -> int {
+    with_kernel<V>(a.dynamic != 0, [&](auto kspmv, auto kspmv0, auto kdec) -> int {
         if (decode_only)
             kdec<<<h->ctas, h->threads, h->smem, st>>>(a);
         else if (y != nullptr)
@@ -250,18 +259,20 @@ int launch(dtans_dev *h, const V *x, const V *y, V *out, const int64_t *row_star
         return 0;
     });
     h->launches++;
-    if (a.ntasks) {
+    if (a.nlong) {
         if (decode_only) {
-            dev::dtans_task_kernel<V, true><<<h->task_ctas, 512, h->task_smem, st>>>(a);
-            h->launches++;
+            if (a.ntasks) dev::dtans_task_kernel<V, true><<<h->task_ctas, 512, h->task_smem, st>>>(a);
+            if (a.nsolo) dev::dtans_solo_kernel<V, true><<<h->solo_ctas, 256, h->task_smem, st>>>(a);
+            h->launches += (a.ntasks ? 1 : 0) + (a.nsolo ? 1 : 0);
         } else {
-            dev::dtans_task_kernel<V, false><<<h->task_ctas, 512, h->task_smem, st>>>(a);
-            const unsigned nb = (a.nlong * 32u + 255u) / 256u;
+            if (a.ntasks) dev::dtans_task_kernel<V, false><<<h->task_ctas, 512, h->task_smem, st>>>(a);
+            if (a.nsolo) dev::dtans_solo_kernel<V, false><<<h->solo_ctas, 256, h->task_smem, st>>>(a);
+            const unsigned nb = a.nlong;
             if (y != nullptr)
                 dev::dtans_finalize_kernel<V, true><<<nb, 256, 0, st>>>(a);
             else
                 dev::dtans_finalize_kernel<V, false><<<nb, 256, 0, st>>>(a);
-            h->launches += 2;
+            h->launches += (a.ntasks ? 1 : 0) + (a.nsolo ? 1 : 0) + 1;
         }
     }
     CK(cudaGetLastError(), "kernel launch");
@@ -301,13 +312,24 @@ extern "C" int dtans_upload(const dtans_container_view *c, int device, dtans_dev
     {
         const char *e1 = getenv("DTANS_LONG_SEG"), *e2 = getenv("DTANS_CHUNK");
         const int long_seg = e1 ? atoi(e1) : 64, chunk = e2 ? atoi(e2) : 32;
-        const int rc0 = build_long_index(c, long_seg, std::max(1, chunk), li);
+        // slices whose stream window cannot be staged in a ring buffer go to
+        // the task kernels as well (their words would be read uncached)
+        int max_optin = 0;
+        if (cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device) != cudaSuccess)
+            max_optin = 227 * 1024;
+        const int64_t fixed = (int64_t)tb.words.size() * 4 + dev::kMaxWarps * dev::kRing * (8 + sizeof(dev::SliceMeta)) +
+                              256 + dev::kOverrunWords * 4;
+        const uint64_t max_words = (uint64_t)std::max<int64_t>(4, (max_optin - fixed) / (dev::kMaxWarps * dev::kRing * 4) / 4 * 4);
+        const int rc0 = build_long_index(c, long_seg, max_words, std::max(1, chunk), li);
         if (rc0) {
             delete h;
             return rc0;
         }
-        h->base.long_seg = li.tasks.empty() ? 0xFFFFFFFFu : (uint32_t)long_seg;
+        h->base.long_seg = li.slices.empty() ? 0xFFFFFFFFu : (uint32_t)long_seg;
+        h->long_words = max_words;
+        h->base.long_words = li.slices.empty() ? 0xFFFFFFFFu : (uint32_t)std::min<uint64_t>(max_words, 0xFFFFFFFEull);
         h->base.ntasks = (uint32_t)li.tasks.size();
+        h->base.nsolo = (uint32_t)li.solo.size();
         h->base.nlong = (uint32_t)li.slices.size();
     }
 
@@ -317,7 +339,7 @@ extern "C" int dtans_upload(const dtans_container_view *c, int device, dtans_dev
     const size_t o_rs = off; off = align_up(off + sizeof(uint32_t) * (size_t)std::max<int64_t>(c->rows, 1), 256);
     const size_t o_di = off; off = align_up(off + sizeof(uint64_t) * (size_t)(nsl + 1), 256);
     const size_t o_st = off; off = align_up(off + sizeof(uint32_t) * ((size_t)c->nwords + dev::kOverrunWords), 256);
-    const size_t o_er = off; off = align_up(off + 16, 256);
+    const size_t o_er = off; off = align_up(off + 64, 256);
     cudaError_t e = cudaMalloc(&h->d_base, off);
     if (e != cudaSuccess) {
         delete h;
@@ -343,11 +365,12 @@ extern "C" int dtans_upload(const dtans_container_view *c, int device, dtans_dev
     cp(h->d_stream, c->stream, sizeof(uint32_t) * (size_t)c->nwords);
     if (rc == DTANS_OK) {
         cudaError_t ce = cudaMemset(h->d_stream + c->nwords, 0, sizeof(uint32_t) * dev::kOverrunWords);
-        if (ce == cudaSuccess) ce = cudaMemset(h->d_err, 0, 16);
+        if (ce == cudaSuccess) ce = cudaMemset(h->d_err, 0, 64);
         if (ce != cudaSuccess) rc = cuda_fail(ce, "memset");
     }
-    if (rc == DTANS_OK && !li.tasks.empty()) {
-        const size_t tb_b = align_up(li.tasks.size() * sizeof(LongTask), 256);
+    if (rc == DTANS_OK && !li.slices.empty()) {
+        const size_t tb_b = align_up(li.tasks.size() * sizeof(LongTask), 256) +
+                            align_up(li.solo.size() * sizeof(SoloTask), 256);
         const size_t pl_b = align_up(li.pool.size() * 4, 256);
         const size_t ls_b = align_up(li.slices.size() * sizeof(LongSlice), 256);
         const size_t pa_b = align_up((size_t)li.nparts * 32 * c->precision, 256);
@@ -358,12 +381,52 @@ extern "C" int dtans_upload(const dtans_container_view *c, int device, dtans_dev
         } else {
             char *lb = (char *)h->d_long;
             h->base.tasks = (const LongTask *)lb;
+            h->base.solo = (const SoloTask *)(lb + align_up(li.tasks.size() * sizeof(LongTask), 256));
             h->base.ck_pool = (const uint32_t *)(lb + tb_b);
             h->base.longs = (const LongSlice *)(lb + tb_b + pl_b);
             h->base.partials = lb + tb_b + pl_b + ls_b;
             cp(lb, li.tasks.data(), li.tasks.size() * sizeof(LongTask));
+            cp((void *)h->base.solo, li.solo.data(), li.solo.size() * sizeof(SoloTask));
+            if (rc == DTANS_OK) {
+                // partial slots of solo tasks are written for one lane only
+                cudaError_t me = cudaMemset(h->base.partials, 0, pa_b);
+                if (me != cudaSuccess) rc = cuda_fail(me, "memset partials");
+            }
             cp(lb + tb_b, li.pool.data(), li.pool.size() * 4);
             cp(lb + tb_b + pl_b, li.slices.data(), li.slices.size() * sizeof(LongSlice));
+        }
+    }
+    if (rc == DTANS_OK && nsl > 0) {
+        // skewed slice costs -> dynamic longest-first scheduling
+        std::vector<uint32_t> cost((size_t)nsl);
+        double mean = 0;
+        uint32_t mx = 0;
+        for (int64_t s = 0; s < nsl; s++) {
+            uint32_t m = 0;
+            for (int64_t i = s * kSlice; i < std::min<int64_t>((s + 1) * kSlice, c->rows); i++)
+                m = std::max(m, c->row_symbols[i]);
+            cost[s] = (m + 7) / 8;
+            const uint64_t words = ((c->directory[s + 1] + 3) & ~3ull) - (c->directory[s] & ~3ull);
+            if (cost[s] > h->base.long_seg || words > h->long_words) cost[s] = 0;  // task-decoded
+            mean += cost[s];
+            mx = std::max(mx, cost[s]);
+        }
+        mean /= (double)nsl;
+        const char *ed = getenv("DTANS_DYNAMIC");
+        const bool dyn = ed ? atoi(ed) != 0 : (mx > 4.0 * std::max(mean, 1.0));
+        h->base.dynamic = dyn ? 1 : 0;
+        bool sorted = true;
+        for (int64_t s = 1; s < nsl && sorted; s++) sorted = cost[s] <= cost[s - 1];
+        if (dyn && !sorted) {
+            std::vector<uint32_t> order((size_t)nsl);
+            for (int64_t s = 0; s < nsl; s++) order[s] = (uint32_t)s;
+            std::stable_sort(order.begin(), order.end(), [&](uint32_t p, uint32_t q) { return cost[p] > cost[q]; });
+            cudaError_t ce = cudaMalloc(&h->d_order, sizeof(uint32_t) * order.size());
+            if (ce != cudaSuccess) rc = cuda_fail(ce, "cudaMalloc slice order");
+            else {
+                cp(h->d_order, order.data(), sizeof(uint32_t) * order.size());
+                h->base.slice_order = h->d_order;
+            }
         }
     }
     if (rc == DTANS_OK)
@@ -371,6 +434,7 @@ extern "C" int dtans_upload(const dtans_container_view *c, int device, dtans_dev
     if (rc != DTANS_OK) {
         cudaFree(h->d_base);
         if (h->d_long) cudaFree(h->d_long);
+        if (h->d_order) cudaFree(h->d_order);
         delete h;
         return rc;
     }
@@ -384,6 +448,8 @@ extern "C" void dtans_free(dtans_dev *h)
     cudaSetDevice(h->device);
     if (h->d_base) cudaFree(h->d_base);
     if (h->d_long) cudaFree(h->d_long);
+    if (h->d_row_map) cudaFree(h->d_row_map);
+    if (h->d_order) cudaFree(h->d_order);
     if (h->d_io) cudaFree(h->d_io);
     delete h;
 }
@@ -396,6 +462,28 @@ extern "C" int dtans_info(const dtans_dev *h, int64_t *device_bytes, int32_t *ct
     if (ctas) *ctas = h->ctas;
     if (warps_per_cta) *warps_per_cta = h->threads / 32;
     if (smem_bytes) *smem_bytes = h->smem;
+    return DTANS_OK;
+}
+
+extern "C" int dtans_set_row_map(dtans_dev *h, const uint32_t *host_map)
+{
+    if (!h) return fail(DTANS_E_PARAM, "null handle");
+    CK(cudaSetDevice(h->device), "cudaSetDevice");
+    if (!host_map) {
+        if (h->d_row_map) cudaFree(h->d_row_map);
+        h->d_row_map = nullptr;
+        h->base.row_map = nullptr;
+        return DTANS_OK;
+    }
+    std::vector<uint8_t> seen((size_t)h->rows, 0);
+    for (int64_t i = 0; i < h->rows; i++) {
+        if (host_map[i] >= (uint64_t)h->rows || seen[host_map[i]])
+            return fail(DTANS_E_PARAM, "row map must be a permutation of [0, rows)");
+        seen[host_map[i]] = 1;
+    }
+    if (!h->d_row_map) CK(cudaMalloc(&h->d_row_map, sizeof(uint32_t) * (size_t)std::max<int64_t>(h->rows, 1)), "cudaMalloc row map");
+    CK(cudaMemcpy(h->d_row_map, host_map, sizeof(uint32_t) * (size_t)h->rows, cudaMemcpyHostToDevice), "upload row map");
+    h->base.row_map = h->d_row_map;
     return DTANS_OK;
 }
 

@@ -66,7 +66,8 @@ void parse_tables(const uint8_t *recs, int precision, HostTables &t)
 // mismatch).  Column deltas need the symbols, so escapes' payloads and the
 // delta dictionary are read like the device does.
 bool walk_slice(const dtans_container_view *c, const HostTables &T, const uint32_t *dsym_tab, int64_t s,
-                int chunk, std::vector<uint32_t> &pool, std::vector<LongTask> &tasks, uint32_t part_base)
+                int chunk, std::vector<uint32_t> &pool, std::vector<LongTask> &tasks, std::vector<SoloTask> &solo,
+                uint32_t part_base)
 {
     const int64_t row0 = s * kSlice;
     const int nl = (int)std::min<int64_t>(kSlice, c->rows - row0);
@@ -96,8 +97,33 @@ bool walk_slice(const dtans_container_view *c, const HostTables &T, const uint32
         if (nseg[i] && !fetch(w2[i])) return false;
     const uint32_t ntasks = (max_nseg + chunk - 1) / chunk;
     uint32_t k = 0;
+    const size_t first_task = tasks.size(), first_solo = solo.size();
     for (uint32_t j = 0; j < max_nseg; j++) {
-        if (j % chunk == 0) {
+        uint32_t amask = 0;
+        if (j % chunk == 0 && j)
+            for (int i = 0; i < nl; i++)
+                if (nseg[i] > j) amask |= 1u << i;
+        if (j % chunk == 0 && j && __builtin_popcount(amask) == 1) {
+            // one lane left: its remaining words are consecutive (solo task)
+            const int i = __builtin_ctz(amask);
+            SoloTask t;
+            t.slice = (uint32_t)s;
+            t.lane = (uint32_t)i;
+            t.j0 = j;
+            t.j1 = std::min<uint32_t>(j + chunk, max_nseg);
+            t.part = part_base + k;
+            t.cur0 = (uint32_t)cur;
+            t.cur1 = 0;
+            t.ck = (uint32_t)pool.size();
+            pool.push_back(w0[i]);
+            pool.push_back(w1[i]);
+            pool.push_back(w2[i]);
+            pool.push_back(d[i]);
+            pool.push_back(r[i]);
+            pool.push_back(col[i]);
+            solo.push_back(t);
+            k++;
+        } else if (j % chunk == 0) {
             // task k covers segments [j, min(j + chunk, max_nseg))
             LongTask t;
             t.slice = (uint32_t)s;
@@ -175,15 +201,27 @@ bool walk_slice(const dtans_container_view *c, const HostTables &T, const uint32
             if (j + 1 < nseg[i] && !fetch(w2[i])) return false;
         // the next task's start cursor
     }
-    // expected cursor at each task end = next task's cur0, last = nwords
-    for (size_t t = tasks.size() - ntasks; t < tasks.size(); t++)
-        tasks[t].cur1 = t + 1 < tasks.size() ? tasks[t + 1].cur0 : (uint32_t)nw;
+    // expected cursor at each task end = the next task's start, last = nwords
+    // (warp tasks precede the solo tasks of the same slice)
+    std::vector<uint32_t *> ends;
+    std::vector<uint32_t> starts;
+    for (size_t t = first_task; t < tasks.size(); t++) {
+        ends.push_back(&tasks[t].cur1);
+        starts.push_back(tasks[t].cur0);
+    }
+    for (size_t t = first_solo; t < solo.size(); t++) {
+        ends.push_back(&solo[t].cur1);
+        starts.push_back(solo[t].cur0);
+    }
+    for (size_t q = 0; q < ends.size(); q++) *ends[q] = q + 1 < ends.size() ? starts[q + 1] : (uint32_t)nw;
+    (void)ntasks;
     return cur == nw;
 }
 
 }  // namespace
 
-int build_long_index(const dtans_container_view *c, int seg_threshold, int chunk, LongIndex &out)
+int build_long_index(const dtans_container_view *c, int seg_threshold, uint64_t max_words, int chunk,
+                     LongIndex &out)
 {
     out = LongIndex();
     const int64_t nsl = c->nslices;
@@ -192,7 +230,8 @@ int build_long_index(const dtans_container_view *c, int seg_threshold, int chunk
         const int64_t row0 = s * kSlice, row1 = std::min<int64_t>(row0 + kSlice, c->rows);
         uint32_t mx = 0;
         for (int64_t i = row0; i < row1; i++) mx = std::max(mx, c->row_symbols[i]);
-        if ((mx + 7) / 8 > (uint32_t)seg_threshold) longs.push_back((uint32_t)s);
+        const uint64_t words = ((c->directory[s + 1] + 3) & ~3ull) - (c->directory[s] & ~3ull);
+        if ((mx + 7) / 8 > (uint32_t)seg_threshold || words > max_words) longs.push_back((uint32_t)s);
     }
     if (longs.empty()) return DTANS_OK;
     HostTables T;
@@ -215,6 +254,7 @@ int build_long_index(const dtans_container_view *c, int seg_threshold, int chunk
     const int nt = std::max(1, std::min<int>((int)std::thread::hardware_concurrency(), (int)longs.size()));
     std::vector<std::vector<uint32_t>> pools(nt);
     std::vector<std::vector<LongTask>> tasks(nt);
+    std::vector<std::vector<SoloTask>> solos(nt);
     std::atomic<size_t> next{0};
     std::atomic<int> bad{0};
     std::vector<std::thread> th;
@@ -223,7 +263,7 @@ int build_long_index(const dtans_container_view *c, int seg_threshold, int chunk
             for (;;) {
                 const size_t i = next.fetch_add(1);
                 if (i >= longs.size()) break;
-                if (!walk_slice(c, T, dsym.data(), longs[i], chunk, pools[t], tasks[t], base[i])) bad = 1;
+                if (!walk_slice(c, T, dsym.data(), longs[i], chunk, pools[t], tasks[t], solos[t], base[i])) bad = 1;
             }
         });
     for (auto &x : th) x.join();
@@ -234,11 +274,17 @@ int build_long_index(const dtans_container_view *c, int seg_threshold, int chunk
             if (tk.ck != 0xFFFFFFFFu) tk.ck += off;
             out.tasks.push_back(tk);
         }
+        for (auto tk : solos[t]) {
+            tk.ck += off;
+            out.solo.push_back(tk);
+        }
         out.pool.insert(out.pool.end(), pools[t].begin(), pools[t].end());
     }
     // longest tasks first (LPT) so the tail of the task kernel is short
     std::stable_sort(out.tasks.begin(), out.tasks.end(),
                      [](const LongTask &a, const LongTask &b) { return a.j1 - a.j0 > b.j1 - b.j0; });
+    std::stable_sort(out.solo.begin(), out.solo.end(),
+                     [](const SoloTask &a, const SoloTask &b) { return a.j1 - a.j0 > b.j1 - b.j0; });
     for (size_t i = 0; i < longs.size(); i++)
         out.slices.push_back(LongSlice{longs[i], base[i], base[i + 1] - base[i], 0});
     out.nparts = base.back();

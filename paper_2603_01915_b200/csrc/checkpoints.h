@@ -16,12 +16,21 @@ struct LongTask {
     uint32_t ck, last;             // last: j1 is the slice's final segment count
 };
 
+// Segments [j0, j1) of a long slice whose only active lane is `lane` from
+// j0 on: its words are consecutive in the stream, so one thread decodes the
+// chunk without the other lanes.  ck indexes {w0, w1, w2, d, r, col}.
+struct SoloTask {
+    uint32_t slice, lane, j0, j1;
+    uint32_t part, cur0, cur1, ck;
+};
+
 struct LongSlice {
     uint32_t slice, part_base, nparts, pad;
 };
 
 struct LongIndex {
     std::vector<LongTask> tasks;
+    std::vector<SoloTask> solo;
     std::vector<uint32_t> pool;
     std::vector<LongSlice> slices;
     uint32_t nparts = 0;
@@ -29,6 +38,10 @@ struct LongIndex {
 
 // Slices whose longest row has more than seg_threshold segments are split
 // into tasks of `chunk` segments.
-int build_long_index(const dtans_container_view *c, int seg_threshold, int chunk, LongIndex &out);
+// Slices whose longest row has more than seg_threshold segments, or whose
+// 16-byte aligned stream window exceeds max_words (does not fit a staging
+// buffer), are split into tasks of `chunk` segments.
+int build_long_index(const dtans_container_view *c, int seg_threshold, uint64_t max_words, int chunk,
+                     LongIndex &out);
 
 }  // namespace dtans

@@ -78,11 +78,18 @@ struct KernelArgs {
     unsigned int *err;            // bit 0: consumption mismatch, bit 1: column OOB
     // long slices (checkpoint index, checkpoints.cpp)
     uint32_t long_seg;            // slices with more segments go to the task kernel
-    uint32_t ntasks, nlong;
+    uint32_t long_words;          // ... and slices with more stream words
+    uint32_t ntasks, nlong, nsolo;
     const LongTask *tasks;
+    const SoloTask *solo;
     const uint32_t *ck_pool;
     const LongSlice *longs;
     void *partials;               // V[nparts][32]
+    const uint32_t *row_map;      // optional: y/out index of encoded row i (row-reordered P*A)
+    // work distribution
+    int32_t dynamic;              // 1: atomic ticket counter instead of a static stride
+    uint32_t *work_counter;       // zeroed before every dynamic launch
+    const uint32_t *slice_order;  // optional: ticket -> slice (longest first)
 };
 
 __device__ __forceinline__ uint32_t lanemask_lt()
@@ -200,20 +207,28 @@ struct GmemSrc {
 struct SliceMeta {
     uint32_t off;     // words from the window start to directory[s]; bit 31 = global
     uint32_t nwords;  // directory[s+1] - directory[s]
+    uint32_t slice;   // slice id (kNoSlice: the warp's work is exhausted)
+    uint32_t pad;
 };
+constexpr uint32_t kNoSlice = 0xFFFFFFFFu;
 constexpr uint32_t kGlobalSlice = 0x80000000u;
 
 // Stage a slice (directory entries lo, hi prefetched) into a ring buffer
 // (lane 0 only).  The previous contents were consumed by this warp's LDS
 // before the __syncwarp that precedes the call (the same WAR ordering a
 // CUTLASS TMA pipeline relies on), so no proxy fence is issued.
-__device__ __forceinline__ void stage_slice(const KernelArgs &a, uint64_t lo, uint64_t hi, uint64_t *bar,
-                                            SliceMeta *meta, uint32_t *buf)
+__device__ __forceinline__ void stage_slice(const KernelArgs &a, uint32_t s, uint64_t lo, uint64_t hi,
+                                            uint64_t *bar, SliceMeta *meta, uint32_t *buf)
 {
+    if (s == kNoSlice) {
+        *meta = SliceMeta{0u, 0u, kNoSlice, 0u};
+        mbar_arrive(bar);
+        return;
+    }
     const uint64_t abase = lo & ~3ull;
     const uint32_t words = (uint32_t)(((hi + 3) & ~3ull) - abase);
     const bool staged = words > 0 && words <= (uint32_t)a.bufw;
-    *meta = SliceMeta{(uint32_t)(lo - abase) | (staged ? 0u : kGlobalSlice), (uint32_t)(hi - lo)};
+    *meta = SliceMeta{(uint32_t)(lo - abase) | (staged ? 0u : kGlobalSlice), (uint32_t)(hi - lo), s, 0u};
     if (staged) {
         mbar_arrive_expect_tx(bar, words * 4u);
         bulk_g2s(buf, a.stream + abase, words * 4u, bar);
@@ -562,9 +577,10 @@ __device__ __forceinline__ void decode_slice(const KernelArgs &a, const Ctx &C, 
     using T = ValueTraits<V>;
     const uint32_t maxn = __reduce_max_sync(0xFFFFFFFFu, n);
     const uint32_t max_nseg = (maxn + 7u) >> 3;
-    if (max_nseg > a.long_seg) return;  // long slice: decoded by the task kernel (uniform)
+    if (max_nseg > a.long_seg) return;  // task-decoded slice (uniform)
+    const uint32_t orow = (a.row_map != nullptr && inrow) ? __ldg(a.row_map + row) : row;
     V yv = V(0);
-    if (kHasY) yv = __ldg(reinterpret_cast<const V *>(a.y) + (inrow ? row : 0u));
+    if (kHasY) yv = __ldg(reinterpret_cast<const V *>(a.y) + (inrow ? orow : 0u));
     LaneState<V> st;
     st.out_pos = 0;
     if (kDecode && inrow) st.out_pos = __ldg(a.row_start + row);
@@ -573,7 +589,7 @@ __device__ __forceinline__ void decode_slice(const KernelArgs &a, const Ctx &C, 
     report(a, C, ok, st.cur, end, n, st.col, lane);
     if (!kDecode && inrow) {
         const V res = kHasY ? T::add(st.acc, yv) : st.acc;
-        reinterpret_cast<V *>(a.out)[row] = res;
+        reinterpret_cast<V *>(a.out)[orow] = res;
     }
 }
 
@@ -582,7 +598,7 @@ __device__ __forceinline__ void decode_slice(const KernelArgs &a, const Ctx &C, 
 // and writes its 32 per-lane partial sums (or, when decoding, the columns
 // and value bits of those segments directly).
 template <typename V, bool kDecode>
-__global__ void __launch_bounds__(512, 1) dtans_task_kernel(const KernelArgs a)
+__global__ void __launch_bounds__(512, 2) dtans_task_kernel(const KernelArgs a)
 {
     using Bits = typename ValueTraits<V>::Bits;
     extern __shared__ __align__(128) unsigned char smem[];
@@ -640,27 +656,155 @@ __global__ void __launch_bounds__(512, 1) dtans_task_kernel(const KernelArgs a)
     }
 }
 
-// Long-slice rows: y' = ((p_0 + p_1) + ... + p_k) + y, partials in task order.
-template <typename V, bool kHasY>
-__global__ void dtans_finalize_kernel(const KernelArgs a)
+// Solo tasks: one THREAD decodes segments [j0, j1) of the only row still
+// active in its long slice.  With a single active lane every event of the
+// slice belongs to that row (container.py:406-413 with one lane), so its
+// words are consecutive from cur0 and the lockstep ballots reduce to a
+// running cursor; 32 independent chunks share a warp.
+template <typename V, bool kDecode>
+__global__ void __launch_bounds__(256) dtans_solo_kernel(const KernelArgs a)
 {
     using T = ValueTraits<V>;
-    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= a.nlong * 32u) return;
-    const LongSlice ls = a.longs[i >> 5];
-    const uint32_t lane = i & 31u;
-    const uint32_t row = ls.slice * kSliceRows + lane;
-    if (row >= (uint32_t)a.rows) return;
-    const V *part = reinterpret_cast<const V *>(a.partials);
-    V acc = part[(size_t)ls.part_base * 32 + lane];
-    for (uint32_t k = 1; k < ls.nparts; k++) acc = T::add(acc, part[(size_t)(ls.part_base + k) * 32 + lane]);
-    if (kHasY) acc = T::add(acc, reinterpret_cast<const V *>(a.y)[row]);
-    reinterpret_cast<V *>(a.out)[row] = acc;
+    using Bits = typename T::Bits;
+    extern __shared__ __align__(128) unsigned char smem[];
+    {
+        const int4 *srcv = reinterpret_cast<const int4 *>(a.tables);
+        int4 *dst = reinterpret_cast<int4 *>(smem);
+        for (int i = threadIdx.x; i < a.table_bytes / 16; i += blockDim.x) dst[i] = __ldg(srcv + i);
+    }
+    __syncthreads();
+    const uint32_t sbase = smem_u32(smem);
+    const uint32_t dtab = sbase, vtab = sbase + kSlots * 4;
+    const uint32_t ddict = sbase + (uint32_t)a.off_ddict, vdict = sbase + (uint32_t)a.off_vdict;
+    const uint32_t cols_m1 = (uint32_t)(a.cols - 1);
+    const V *__restrict__ x = reinterpret_cast<const V *>(a.x);
+    for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < a.nsolo; t += gridDim.x * blockDim.x) {
+        const SoloTask tk = a.solo[t];
+        const uint32_t row = tk.slice * kSliceRows + tk.lane;
+        const uint32_t n = __ldg(a.row_symbols + row);
+        const uint32_t nseg = (n + 7u) >> 3;
+        const uint32_t *__restrict__ st = a.stream + __ldg(a.directory + tk.slice);
+        const uint32_t *ck = a.ck_pool + tk.ck;
+        uint32_t w0 = __ldg(ck), w1 = __ldg(ck + 1), w2 = __ldg(ck + 2), d = __ldg(ck + 3), r = __ldg(ck + 4);
+        uint32_t col = __ldg(ck + 5), cur = tk.cur0;
+        int64_t out_pos = kDecode ? __ldg(a.row_start + row) + 4ll * tk.j0 : 0;
+        V acc = V(0);
+        bool ok = true;
+        for (uint32_t j = tk.j0; j < tk.j1; j++) {
+            uint32_t so[8], e[8], ds[4];
+            Bits vs[4];
+            slot_offsets(w0, w1, w2, so);
+#pragma unroll
+            for (int p = 0; p < 4; p++) {
+                e[2 * p] = lds32(dtab + so[2 * p]);
+                e[2 * p + 1] = lds32(vtab + so[2 * p + 1]);
+                ds[p] = lds32(ddict + (e[2 * p] >> 16));
+                vs[p] = lds_bits<Bits>(vdict + (e[2 * p + 1] >> 16));
+            }
+#pragma unroll
+            for (int p = 0; p < 4; p++) {  // payloads in slot order, low word first
+                if (e[2 * p] >= a.desc_min) ds[p] = __ldg(st + cur++);
+                if (e[2 * p + 1] >= a.vesc_min) {
+                    if (T::kPayloadWords == 2) {
+                        const uint32_t lo = __ldg(st + cur), hi = __ldg(st + cur + 1);
+                        vs[p] = (Bits)(((unsigned long long)hi << 32) | lo);
+                    } else {
+                        vs[p] = (Bits)__ldg(st + cur);
+                    }
+                    cur += T::kPayloadWords;
+                }
+            }
+#pragma unroll
+            for (int p = 0; p < 4; p++) {
+                if (8u * j + 2u * p < n) {
+                    col += ds[p];
+                    if (kDecode) {
+                        a.dec_cols[out_pos] = (int64_t)col;
+                        reinterpret_cast<Bits *>(a.dec_vals)[out_pos] = vs[p];
+                        out_pos++;
+                    } else {
+                        acc = T::add(acc, T::mul(T::from_bits(vs[p]), __ldg(x + min(col, cols_m1))));
+                    }
+                }
+            }
+            if (j + 1 < nseg) {
+                uint32_t bm1a, dga, bm1b, dgb, lo, hi;
+                group(e[0], e[1], e[2], e[3], bm1a, dga);
+                group(e[4], e[5], e[6], e[7], bm1b, dgb);
+                mad_wide(r, bm1a, r, 0u, lo, hi);
+                uint32_t dl, dh;
+                fold(d, bm1a, dga, dl, dh);
+                if (hi) {
+                    w0 = dl;
+                    d = dh;
+                    r = hi;
+                } else {
+                    w0 = __ldg(st + cur++);
+                    d = dl;
+                    r = lo;
+                }
+                mad_wide(r, bm1b, r, 0u, lo, hi);
+                fold(d, bm1b, dgb, dl, dh);
+                if (hi) {
+                    w1 = dl;
+                    d = dh;
+                    r = hi;
+                } else {
+                    w1 = __ldg(st + cur++);
+                    d = dl;
+                    r = lo;
+                }
+                w2 = __ldg(st + cur++);
+            }
+            if (cur > tk.cur1) {
+                ok = false;
+                break;
+            }
+        }
+        if (!ok || cur != tk.cur1 || (tk.j1 == nseg && col > cols_m1)) atomicOr(a.err, !ok || cur != tk.cur1 ? 1u : 2u);
+        if (!kDecode) reinterpret_cast<V *>(a.partials)[(size_t)tk.part * 32 + tk.lane] = acc;
+    }
 }
+
+// Long-slice rows: y' = (sum of the row's task partials) + y.  One CTA of
+// 8 warps per long slice: warp w adds the partials k = w, w+8, ... of all 32
+// rows (lane = row, coalesced), then the 8 warp sums are added in warp order:
+// a fixed order, so the result is deterministic.
+template <typename V, bool kHasY>
+__global__ void __launch_bounds__(256) dtans_finalize_kernel(const KernelArgs a)
+{
+    using T = ValueTraits<V>;
+    __shared__ V red[8][32];
+    const LongSlice ls = a.longs[blockIdx.x];
+    const uint32_t lane = threadIdx.x & 31u, w = threadIdx.x >> 5;
+    const V *part = reinterpret_cast<const V *>(a.partials) + (size_t)ls.part_base * 32 + lane;
+    V acc = V(0);
+    uint32_t k = w;
+    for (; k + 24 < ls.nparts; k += 32) {
+        const V p0 = part[(size_t)k * 32], p1 = part[(size_t)(k + 8) * 32];
+        const V p2 = part[(size_t)(k + 16) * 32], p3 = part[(size_t)(k + 24) * 32];
+        acc = T::add(acc, T::add(T::add(p0, p1), T::add(p2, p3)));
+    }
+    for (; k < ls.nparts; k += 8) acc = T::add(acc, part[(size_t)k * 32]);
+    red[w][lane] = acc;
+    __syncthreads();
+    if (w == 0) {
+        V s = red[0][lane];
+#pragma unroll
+        for (int q = 1; q < 8; q++) s = T::add(s, red[q][lane]);
+        const uint32_t row = ls.slice * kSliceRows + lane;
+        if (row < (uint32_t)a.rows) {
+            const uint32_t orow = a.row_map != nullptr ? __ldg(a.row_map + row) : row;
+            if (kHasY) s = T::add(s, reinterpret_cast<const V *>(a.y)[orow]);
+            reinterpret_cast<V *>(a.out)[orow] = s;
+        }
+    }
+}
+
 
 // Persistent kernel, one CTA of 32 warps per SM: tables -> shared memory once,
 // then every warp walks its slices (grid-wide stride) through its TMA ring.
-template <typename V, bool kDecode, bool kHasY, int kThreads>
+template <typename V, bool kDecode, bool kHasY, bool kDyn, int kThreads>
 __global__ void __launch_bounds__(kThreads, 1) dtans_kernel(const KernelArgs a)
 {
     constexpr int kWarps = kThreads / 32;
@@ -697,33 +841,104 @@ __global__ void __launch_bounds__(kThreads, 1) dtans_kernel(const KernelArgs a)
     const uint32_t rows = (uint32_t)a.rows;  // < 2^32 (checked at upload)
     const uint32_t first = blockIdx.x * kWarps + warp;
     const uint32_t stride = gridDim.x * kWarps;
-    if (lane == 0)
-        for (int b = 0; b < kRing; b++) {
-            const uint32_t s = first + b * stride;
-            if (s < nsl)
-                stage_slice(a, __ldg(a.directory + s), __ldg(a.directory + s + 1), &bars[b], &meta[b],
-                            bufs + b * a.bufw);
+    if constexpr (!kDyn) {
+        // static order: slices first, first + stride, ...
+        if (lane == 0)
+            for (int b = 0; b < kRing; b++) {
+                const uint32_t s = first + b * stride;
+                if (s < nsl)
+                    stage_slice(a, s, __ldg(a.directory + s), __ldg(a.directory + s + 1), &bars[b], &meta[b],
+                                bufs + b * a.bufw);
+            }
+        uint32_t n_next = 0;
+        if (first < nsl && first * kSliceRows + lane < rows)
+            n_next = __ldg(a.row_symbols + first * kSliceRows + lane);
+        int b = 0;
+        uint32_t parity = 0;
+        for (uint32_t s = first; s < nsl; s += stride) {
+            const uint32_t n = n_next;
+            const uint32_t sn = s + stride;
+            n_next = (sn < nsl && sn * kSliceRows + lane < rows) ? __ldg(a.row_symbols + sn * kSliceRows + lane) : 0u;
+            // directory entries of the slice this buffer is refilled with
+            const uint32_t sr = s + kRing * stride;
+            uint64_t rlo = 0, rhi = 0;
+            if (lane == 0 && sr < nsl) {
+                rlo = __ldg(a.directory + sr);
+                rhi = __ldg(a.directory + sr + 1);
+            }
+            mbar_wait(&bars[b], parity);
+            const SliceMeta md = meta[b];
+            const uint32_t row = s * kSliceRows + lane;
+            const bool inrow = row < rows;
+            const uint32_t aw = ((md.off & ~kGlobalSlice) + md.nwords + 3u) & ~3u;  // aligned window
+            if (aw > a.long_words) {
+                // task-decoded slice (checkpoints.cpp criterion)
+            } else if (!(md.off & kGlobalSlice)) {
+                const SmemSrc src{smem_u32(bufs + b * a.bufw) + md.off * 4u};
+                decode_slice<V, kDecode, kHasY>(a, C, x, src, md.nwords, n, row, inrow, lane);
+            } else {
+                const GmemSrc src{a.stream + __ldg(a.directory + s)};
+                decode_slice<V, kDecode, kHasY>(a, C, x, src, md.nwords, n, row, inrow, lane);
+            }
+            __syncwarp();
+            if (lane == 0 && sr < nsl) stage_slice(a, sr, rlo, rhi, &bars[b], &meta[b], bufs + b * a.bufw);
+            if (++b == kRing) {
+                b = 0;
+                parity ^= 1u;
+            }
         }
-    uint32_t n_next = 0;
-    if (first < nsl && first * kSliceRows + lane < rows) n_next = __ldg(a.row_symbols + first * kSliceRows + lane);
+        return;
+    }
+    // Dynamic order (skewed containers): each claim takes the next ticket of
+    // a global counter, in the longest-first order of a.slice_order; tickets
+    // are claimed kRing slices before they are decoded, so the atomic's
+    // latency is hidden.
+    auto claim = [&]() -> uint32_t {  // lane 0 only
+        const uint32_t p = atomicAdd(a.work_counter, 1u);
+        if (p >= nsl) return kNoSlice;
+        return a.slice_order != nullptr ? __ldg(a.slice_order + p) : p;
+    };
+    if (lane == 0) {
+        for (int b = 0; b < kRing; b++) {
+            const uint32_t s = claim();
+            const uint64_t lo = s != kNoSlice ? __ldg(a.directory + s) : 0, hi = s != kNoSlice ? __ldg(a.directory + s + 1) : 0;
+            stage_slice(a, s, lo, hi, &bars[b], &meta[b], bufs + b * a.bufw);
+        }
+    }
+    __syncwarp();
+    uint32_t s_next = meta[0].slice;
+    uint32_t n_next = (s_next != kNoSlice && s_next * kSliceRows + lane < rows)
+                          ? __ldg(a.row_symbols + s_next * kSliceRows + lane)
+                          : 0u;
     int b = 0;
     uint32_t parity = 0;
-    for (uint32_t s = first; s < nsl; s += stride) {
-        const uint32_t n = n_next;
-        const uint32_t sn = s + stride;
-        n_next = (sn < nsl && sn * kSliceRows + lane < rows) ? __ldg(a.row_symbols + sn * kSliceRows + lane) : 0u;
-        // directory entries of the slice this buffer is refilled with
-        const uint32_t sr = s + kRing * stride;
+    for (;;) {
+        // claim the slice this buffer is refilled with, prefetch its directory entries
+        uint32_t sr = kNoSlice;
         uint64_t rlo = 0, rhi = 0;
-        if (lane == 0 && sr < nsl) {
-            rlo = __ldg(a.directory + sr);
-            rhi = __ldg(a.directory + sr + 1);
+        if (lane == 0) {
+            sr = claim();
+            if (sr != kNoSlice) {
+                rlo = __ldg(a.directory + sr);
+                rhi = __ldg(a.directory + sr + 1);
+            }
         }
         mbar_wait(&bars[b], parity);
         const SliceMeta md = meta[b];
+        const uint32_t s = md.slice;
+        if (s == kNoSlice) break;  // uniform
+        const uint32_t n = n_next;
+        const int bn = b + 1 == kRing ? 0 : b + 1;
+        s_next = meta[bn].slice;
+        n_next = (s_next != kNoSlice && s_next * kSliceRows + lane < rows)
+                     ? __ldg(a.row_symbols + s_next * kSliceRows + lane)
+                     : 0u;
         const uint32_t row = s * kSliceRows + lane;
         const bool inrow = row < rows;
-        if (!(md.off & kGlobalSlice)) {
+        const uint32_t aw = ((md.off & ~kGlobalSlice) + md.nwords + 3u) & ~3u;  // aligned window
+        if (aw > a.long_words) {
+            // task-decoded slice (checkpoints.cpp criterion)
+        } else if (!(md.off & kGlobalSlice)) {
             const SmemSrc src{smem_u32(bufs + b * a.bufw) + md.off * 4u};
             decode_slice<V, kDecode, kHasY>(a, C, x, src, md.nwords, n, row, inrow, lane);
         } else {
@@ -731,11 +946,10 @@ __global__ void __launch_bounds__(kThreads, 1) dtans_kernel(const KernelArgs a)
             decode_slice<V, kDecode, kHasY>(a, C, x, src, md.nwords, n, row, inrow, lane);
         }
         __syncwarp();
-        if (lane == 0 && sr < nsl) stage_slice(a, rlo, rhi, &bars[b], &meta[b], bufs + b * a.bufw);
-        if (++b == kRing) {
-            b = 0;
-            parity ^= 1u;
-        }
+        if (lane == 0) stage_slice(a, sr, rlo, rhi, &bars[b], &meta[b], bufs + b * a.bufw);
+        __syncwarp();
+        b = bn;
+        if (b == 0) parity ^= 1u;
     }
 }
 

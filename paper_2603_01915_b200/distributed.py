@@ -60,6 +60,8 @@ def shard(c: CsrDtansContainer, s_lo: int, s_hi: int) -> CsrDtansContainer:
     same tables and parameters, directory rebased to start at 0."""
     if not (0 <= s_lo <= s_hi <= c.nslices):
         raise ParameterError("bad slice range")
+    if c.row_map is not None:
+        raise ParameterError("sharding a row-reordered container is not supported")
     r0 = s_lo * SLICE_HEIGHT
     r1 = min(s_hi * SLICE_HEIGHT, c.rows)
     r1 = max(r0, r1)

@@ -187,3 +187,31 @@ def reference_spmv(m: CsrMatrix, x: np.ndarray, y: np.ndarray) -> np.ndarray:
             idx = base[:a] + q
             acc[order[:a]] += m.values[idx] * x[m.col_idx[idx]]
     return acc + y
+
+
+def sort_rows_by_length(m: CsrMatrix, window: int | None = None):
+    """Row reordering for skewed matrices (fix A): rows
+    stably sorted by descending length, within windows of ``window`` rows
+    (None: globally), so each 32-row slice holds rows of similar length.
+
+    Returns ``(P*A, perm)`` with ``perm[i]`` = original index of row i of P*A
+    (uint32).  Encode P*A with ``encode_matrix`` (byte-identical to the
+    reference's encoding of P*A) and set ``container.row_map = perm``; the
+    SpMV then reads y and writes y' in the original row order.
+    """
+    nnz_row = np.diff(np.asarray(m.row_start, dtype=np.int64))
+    if window is None or window >= m.rows:
+        perm = np.argsort(-nnz_row, kind="stable")
+    else:
+        if window < 1:
+            raise ParameterError("window must be >= 1")
+        blk = np.arange(m.rows) // window
+        perm = np.lexsort((-nnz_row, blk))
+    perm = perm.astype(np.int64)
+    new_len = nnz_row[perm]
+    row_start = np.zeros(m.rows + 1, dtype=np.int64)
+    np.cumsum(new_len, out=row_start[1:])
+    src = np.repeat(np.asarray(m.row_start[:-1], dtype=np.int64)[perm], new_len) + (
+        np.arange(int(row_start[-1]), dtype=np.int64) - np.repeat(row_start[:-1], new_len))
+    pm = CsrMatrix(m.rows, m.cols, row_start, np.asarray(m.col_idx)[src], np.asarray(m.values)[src])
+    return pm, perm.astype(np.uint32)

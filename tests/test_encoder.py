@@ -97,3 +97,17 @@ def test_tables_api():
     assert t.has_symbol(1) and t.base_of(1) >= 1
     assert t.pad_symbol() in t.retained_symbols()
     assert sum(1 for s in t.symbols if s is P.ESCAPE) == int(t.escape.sum())
+
+
+def test_sort_rows_by_length_is_a_row_permutation():
+    m = synth.rmat(10, 5000, seed=1)
+    for window in (None, 100):
+        pm, perm = P.sort_rows_by_length(m, window)
+        assert sorted(perm.tolist()) == list(range(m.rows))
+        nz = np.diff(m.row_start)
+        assert np.array_equal(np.diff(pm.row_start), nz[perm.astype(np.int64)])
+        for i in (0, 7, m.rows - 1):
+            r = int(perm[i])
+            assert np.array_equal(pm.row_cols(i), m.row_cols(r))
+            assert np.array_equal(pm.row_values(i), m.row_values(r))
+        pm.validate()

@@ -138,3 +138,20 @@ def test_long_slice_tasks_match_oracle(long_seg, monkeypatch):
         s = np.abs(m.values.astype(np.float64)) * np.abs(x.astype(np.float64))[m.col_idx]
         s = np.bincount(np.repeat(np.arange(m.rows), np.diff(m.row_start)), weights=s, minlength=m.rows)
         assert np.all(np.abs(out.astype(np.float64) - ref) <= tol * (s + np.abs(y)))
+
+
+@pytest.mark.parametrize("window", [None, 4096])
+def test_row_reordered_rmat(window):
+    """sort_rows_by_length + row_map: results in the original row order."""
+    m = synth.rmat(14, 150000, seed=11)
+    x, y = synth.vectors(m)
+    pm, perm = P.sort_rows_by_length(m, window)
+    c = P.encode_matrix(pm)
+    c.row_map = perm
+    out = P.spmv(c, x, y)
+    ref_p = O.spmv(O.parse(P.serialize(c)), x, y[perm.astype(np.int64)], threads=8)
+    ref = np.empty_like(ref_p)
+    ref[perm.astype(np.int64)] = ref_p
+    exp_p = np.empty_like(out)
+    exp_p = out[perm.astype(np.int64)]
+    assert G.check_spmv(exp_p, ref_p, pm, x, y[perm.astype(np.int64)])

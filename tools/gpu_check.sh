@@ -5,3 +5,4 @@ summ='import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); 
 python bench.py --no-cpu-baseline --no-cusparse "$@" 2>/dev/null | python -c "$summ"
 python bench.py --config banded27 --scale 0.25 --steps 50 --no-cpu-baseline --no-cusparse "$@" 2>/dev/null | python -c "$summ"
 python bench.py --config rmat --scale 0.125 --steps 20 --no-cpu-baseline --no-cusparse "$@" 2>/dev/null | python -c "$summ"
+python bench.py --config rmat --scale 0.125 --steps 20 --reorder --no-cpu-baseline --no-cusparse "$@" 2>/dev/null | python -c "$summ"
