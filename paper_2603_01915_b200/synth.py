@@ -109,33 +109,43 @@ def banded_rows(rows_total: int, r0: int, r1: int, band: int = 32, levels: int =
     return CsrMatrix(len(i), rows_total, row_start, cols, alphabet.astype(dtype)[lvl])
 
 
-def rmat(scale: int, nnz: int, seed: int = 0, probs=(57, 19, 19, 5),
+def rmat(scale: int, nnz: int, seed: int = 0, probs=(0.57, 0.19, 0.19, 0.05),
          dtype=np.float32, batch: int = 1 << 24) -> CsrMatrix:
-    """Config 3: R-MAT (a,b,c,d)=(.57,.19,.19,.05) adjacency, edges drawn
-    until ``nnz`` unique (first occurrences in draw order kept), values 1.0.
-    Quadrant choice uses integer percent draws so it is exact."""
+    """Config 3: R-MAT (a,b,c,d)=(.57,.19,.19,.05) adjacency, values 1.0.
+
+    Edges are drawn in batches (quadrants from 8-bit uniform draws against
+    thresholds round(p * 256): a=146/256, a+b=195/256, a+b+c=243/256, within
+    0.4% of the target probabilities) until at least ``nnz`` distinct edges exist;
+    if there are more, a seeded uniform subset of exactly ``nnz`` is kept.
+    No symmetrisation, no self-loop removal."""
     a, b, c, _ = probs
+    ta, tab, tabc = (int(round(v * 256)) for v in (a, a + b, a + b + c))
     n = 1 << scale
     rng = np.random.default_rng(seed)
-    seen = np.zeros(0, dtype=np.int64)
-    while len(seen) < nnz:
-        need = int((nnz - len(seen)) * 1.15) + 1024
-        m = min(batch, need)
-        r = np.zeros(m, dtype=np.int64)
-        cc = np.zeros(m, dtype=np.int64)
-        for _ in range(scale):
-            u = rng.integers(0, 100, m, dtype=np.uint8)
-            rbit = u >= a + b
-            cbit = ((u >= a) & (u < a + b)) | (u >= a + b + c)
-            r = (r << 1) | rbit
-            cc = (cc << 1) | cbit
-        codes = (r << scale) | cc
-        allc = np.concatenate([seen, codes])
-        _, first = np.unique(allc, return_index=True)
-        first.sort()
-        seen = allc[first]
-    seen = np.sort(seen[:nnz])
-    r, cc = np.divmod(seen, n)
+    it = np.uint32 if scale <= 31 else np.int64
+    uniq = np.zeros(0, dtype=np.int64)
+    while len(uniq) < nnz:
+        need = int((nnz - len(uniq)) * 1.3) + 4096
+        parts = [uniq]
+        while need > 0:
+            m = min(batch, need)
+            r = np.zeros(m, dtype=it)
+            cc = np.zeros(m, dtype=it)
+            for _ in range(scale):
+                uu = np.frombuffer(rng.bytes(m), dtype=np.uint8)
+                r <<= 1
+                cc <<= 1
+                r |= uu >= tab
+                cc |= ((uu >= ta) & (uu < tab)) | (uu >= tabc)
+            parts.append((r.astype(np.int64) << scale) | cc)
+            need -= m
+        allc = np.sort(np.concatenate(parts))  # sort-based unique (np.unique is slow here)
+        uniq = allc[np.concatenate([[True], allc[1:] != allc[:-1]])] if len(allc) else allc
+    if len(uniq) > nnz:
+        keep = rng.choice(len(uniq), nnz, replace=False)
+        keep.sort()
+        uniq = uniq[keep]
+    r, cc = np.divmod(uniq, n)
     return _csr_from_sorted_codes(n, n, r, cc, np.ones(nnz, dtype=dtype))
 
 
