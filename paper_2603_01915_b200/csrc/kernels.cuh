@@ -302,13 +302,16 @@ __device__ __forceinline__ void payload_event(const Ctx &C, const Src &src, uint
         cur += __popc(any);
         return;
     }
-    uint32_t incl = pc;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t v = __shfl_up_sync(0xFFFFFFFFu, incl, o);
-        if (lane >= o) incl += v;
-    }
-    const uint32_t total = __shfl_sync(0xFFFFFFFFu, incl, 31);
+    // exclusive warp scan of pc (<= 12 words: 4 bit planes), one ballot per
+    // plane: independent ballots instead of a dependent 5-step shuffle chain
+    const uint32_t b1 = __ballot_sync(0xFFFFFFFFu, pc & 2u);
+    const uint32_t b2 = __ballot_sync(0xFFFFFFFFu, pc & 4u);
+    const uint32_t b3 = __ballot_sync(0xFFFFFFFFu, pc & 8u);
+    const uint32_t b0 = __ballot_sync(0xFFFFFFFFu, pc & 1u);
+    const uint32_t excl = __popc(b0 & C.lt) + (__popc(b1 & C.lt) << 1) + (__popc(b2 & C.lt) << 2) +
+                          (__popc(b3 & C.lt) << 3);
+    const uint32_t incl = excl + pc;
+    const uint32_t total = __popc(b0) + (__popc(b1) << 1) + (__popc(b2) << 2) + (__popc(b3) << 3);
     if (pc) {
         uint32_t off = cur + (incl - pc);
 #pragma unroll
