@@ -35,7 +35,7 @@ struct dtans_dev {
     // long-slice checkpoint index
     void *d_long = nullptr;     // tasks + pool + slices + partials
     size_t long_bytes = 0;
-    int task_ctas = 0, task_smem = 0, solo_ctas = 0;
+    int task_ctas = 0, task_smem = 0, solo_ctas = 0, solo_smem = 0;
     uint32_t *d_row_map = nullptr;  // optional output row map (reordered P*A)
     uint32_t *d_order = nullptr;    // optional longest-first slice order (dynamic scheduling)
     uint64_t long_words = ~0ull;    // slices with a larger aligned window are task-decoded
@@ -171,10 +171,11 @@ int configure(dtans_dev *h, const TableBlock &tb, const uint64_t *directory)
     int max_optin = 0, sms = 0;
     if (a.nlong) {
         h->task_smem = (int)align_up((size_t)a.table_bytes, 16);
+        h->solo_smem = (int)align_up((size_t)a.table_bytes, 16);
         CK(cudaFuncSetAttribute(dev::dtans_solo_kernel<V, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                h->task_smem), "cudaFuncSetAttribute");
+                                h->solo_smem), "cudaFuncSetAttribute");
         CK(cudaFuncSetAttribute(dev::dtans_solo_kernel<V, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                h->task_smem), "cudaFuncSetAttribute");
+                                h->solo_smem), "cudaFuncSetAttribute");
         CK(cudaFuncSetAttribute(dev::dtans_task_kernel<V, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 h->task_smem), "cudaFuncSetAttribute");
         CK(cudaFuncSetAttribute(dev::dtans_task_kernel<V, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -186,7 +187,7 @@ int configure(dtans_dev *h, const TableBlock &tb, const uint64_t *directory)
         h->task_ctas = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)nsm * std::max(per, 1),
                                                                     ((int64_t)a.ntasks + 15) / 16));
         int pers = 0;
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pers, dev::dtans_solo_kernel<V, false>, 256, h->task_smem),
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pers, dev::dtans_solo_kernel<V, false>, 256, h->solo_smem),
            "occupancy");
         h->solo_ctas = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)nsm * std::max(pers, 1),
                                                                     ((int64_t)a.nsolo + 255) / 256));
@@ -262,11 +263,11 @@ int launch(dtans_dev *h, const V *x, const V *y, V *out, const int64_t *row_star
     if (a.nlong) {
         if (decode_only) {
             if (a.ntasks) dev::dtans_task_kernel<V, true><<<h->task_ctas, 512, h->task_smem, st>>>(a);
-            if (a.nsolo) dev::dtans_solo_kernel<V, true><<<h->solo_ctas, 256, h->task_smem, st>>>(a);
+            if (a.nsolo) dev::dtans_solo_kernel<V, true><<<h->solo_ctas, 256, h->solo_smem, st>>>(a);
             h->launches += (a.ntasks ? 1 : 0) + (a.nsolo ? 1 : 0);
         } else {
             if (a.ntasks) dev::dtans_task_kernel<V, false><<<h->task_ctas, 512, h->task_smem, st>>>(a);
-            if (a.nsolo) dev::dtans_solo_kernel<V, false><<<h->solo_ctas, 256, h->task_smem, st>>>(a);
+            if (a.nsolo) dev::dtans_solo_kernel<V, false><<<h->solo_ctas, 256, h->solo_smem, st>>>(a);
             const unsigned nb = a.nlong;
             if (y != nullptr)
                 dev::dtans_finalize_kernel<V, true><<<nb, 256, 0, st>>>(a);
@@ -338,7 +339,7 @@ extern "C" int dtans_upload(const dtans_container_view *c, int device, dtans_dev
     const size_t o_tb = off; off = align_up(off + tb.words.size() * 4, 256);
     const size_t o_rs = off; off = align_up(off + sizeof(uint32_t) * (size_t)std::max<int64_t>(c->rows, 1), 256);
     const size_t o_di = off; off = align_up(off + sizeof(uint64_t) * (size_t)(nsl + 1), 256);
-    const size_t o_st = off; off = align_up(off + sizeof(uint32_t) * ((size_t)c->nwords + dev::kOverrunWords), 256);
+    const size_t o_st = off; off = align_up(off + sizeof(uint32_t) * ((size_t)c->nwords + dev::kStreamPadWords), 256);
     const size_t o_er = off; off = align_up(off + 64, 256);
     cudaError_t e = cudaMalloc(&h->d_base, off);
     if (e != cudaSuccess) {
@@ -364,7 +365,7 @@ extern "C" int dtans_upload(const dtans_container_view *c, int device, dtans_dev
     cp(h->d_directory, c->directory, sizeof(uint64_t) * (size_t)(nsl + 1));
     cp(h->d_stream, c->stream, sizeof(uint32_t) * (size_t)c->nwords);
     if (rc == DTANS_OK) {
-        cudaError_t ce = cudaMemset(h->d_stream + c->nwords, 0, sizeof(uint32_t) * dev::kOverrunWords);
+        cudaError_t ce = cudaMemset(h->d_stream + c->nwords, 0, sizeof(uint32_t) * dev::kStreamPadWords);
         if (ce == cudaSuccess) ce = cudaMemset(h->d_err, 0, 64);
         if (ce != cudaSuccess) rc = cuda_fail(ce, "memset");
     }

@@ -192,14 +192,18 @@ template <> __device__ __forceinline__ uint32_t lds_bits<uint32_t>(uint32_t addr
 // outside the allocations.
 constexpr uint32_t kSegMaxWords = 32u * 15u;  // payload 12 + 2 checks + 1 uncond per lane
 constexpr uint32_t kOverrunWords = 3u * 32u + kSegMaxWords + 64u;
+constexpr uint32_t kStreamPadWords = kOverrunWords;  // device stream padding
 struct SmemSrc {
     uint32_t addr;  // shared address of word directory[s]
     __device__ __forceinline__ uint32_t operator()(uint32_t rel) const { return lds32_v(addr + rel * 4u); }
+    __device__ __forceinline__ void advance(uint32_t, int) {}
 };
 struct GmemSrc {
     const uint32_t *p;  // &stream[directory[s]]
     __device__ __forceinline__ uint32_t operator()(uint32_t rel) const { return __ldg(p + rel); }
+    __device__ __forceinline__ void advance(uint32_t, int) {}
 };
+
 
 // Per-buffer slice record written by the stager: the slice's word offset
 // inside the 16-byte aligned staged window (bit 31: not staged, read from
@@ -378,7 +382,7 @@ __device__ __forceinline__ void fold(uint32_t d, uint32_t bm1, uint32_t D, uint3
 // 4 pairs valid, all lanes load/extract), so the per-lane predicates vanish.
 template <typename V, bool kDecode, bool kHot, class Src>
 __device__ __forceinline__ void full_segment(const KernelArgs &a, const Ctx &C, const V *__restrict__ x,
-                                             const Src &src, const uint32_t j, const uint32_t n,
+                                             Src &src, const uint32_t j, const uint32_t n,
                                              const uint32_t nseg, uint32_t &w0, uint32_t &w1, uint32_t &w2,
                                              uint32_t &d, uint32_t &r, uint32_t &cur, uint32_t &col, V &acc,
                                              int64_t &out_pos, const int lane)
@@ -478,7 +482,7 @@ template <typename V> struct LaneState {
 // may escape).  Returns false if the cursor ran past `end` (corrupt slice).
 template <typename V, bool kDecode, class Src>
 __device__ __forceinline__ bool decode_range(const KernelArgs &a, const Ctx &C, const V *__restrict__ x,
-                                             const Src &src, const uint32_t end, const uint32_t n,
+                                             Src &src, const uint32_t end, const uint32_t n,
                                              const uint32_t maxn, const uint32_t j0, const uint32_t j1,
                                              LaneState<V> &st, const int lane)
 {
@@ -494,16 +498,19 @@ __device__ __forceinline__ bool decode_range(const KernelArgs &a, const Ctx &C, 
     uint32_t j = j0;
     const uint32_t jhot = min(jfull, min_nseg > 0 ? min_nseg - 1u : 0u);
     for (; j < jhot; j++) {
+        src.advance(st.cur, lane);
         full_segment<V, kDecode, true>(a, C, x, src, j, n, nseg, st.w0, st.w1, st.w2, st.d, st.r, st.cur, st.col,
                                        st.acc, st.out_pos, lane);
         if (st.cur > end) return false;  // uniform
     }
     for (; j < jfull; j++) {
+        src.advance(st.cur, lane);
         full_segment<V, kDecode, false>(a, C, x, src, j, n, nseg, st.w0, st.w1, st.w2, st.d, st.r, st.cur,
                                         st.col, st.acc, st.out_pos, lane);
         if (st.cur > end) return false;
     }
     if (j1 == max_nseg && max_nseg > 0) {
+        src.advance(st.cur, lane);
         const uint32_t jf = max_nseg - 1;
         const bool act = jf < nseg;
         uint32_t so[8], e[8], ds[4];
@@ -543,7 +550,7 @@ __device__ __forceinline__ bool decode_range(const KernelArgs &a, const Ctx &C, 
 
 // init events (container.py:426-429): 3 words per active lane
 template <typename V, class Src>
-__device__ __forceinline__ void init_state(const Ctx &C, const Src &src, const uint32_t n, LaneState<V> &st)
+__device__ __forceinline__ void init_state(const Ctx &C, Src &src, const uint32_t n, LaneState<V> &st)
 {
     const uint32_t am = __ballot_sync(0xFFFFFFFFu, n > 0);
     const uint32_t cnt = __popc(am), rk = __popc(am & C.lt);
@@ -574,7 +581,7 @@ __device__ __forceinline__ void report(const KernelArgs &a, const Ctx &C, bool o
 
 template <typename V, bool kDecode, bool kHasY, class Src>
 __device__ __forceinline__ void decode_slice(const KernelArgs &a, const Ctx &C, const V *__restrict__ x,
-                                             const Src src, const uint32_t end, const uint32_t n,
+                                             Src src, const uint32_t end, const uint32_t n,
                                              const uint32_t row, const bool inrow, const int lane)
 {
     using T = ValueTraits<V>;
@@ -624,16 +631,16 @@ __global__ void __launch_bounds__(512, 2) dtans_task_kernel(const KernelArgs a)
     C.pads_ok = a.pads_ok != 0;
     const V *__restrict__ x = reinterpret_cast<const V *>(a.x);
     const int lane = threadIdx.x & 31;
+    const uint32_t warp = threadIdx.x >> 5;
     const uint32_t warps = blockDim.x >> 5;
-    for (uint32_t t = blockIdx.x * warps + (threadIdx.x >> 5); t < a.ntasks; t += gridDim.x * warps) {
+    for (uint32_t t = blockIdx.x * warps + warp; t < a.ntasks; t += gridDim.x * warps) {
         const LongTask tk = a.tasks[t];
         const uint32_t row = tk.slice * kSliceRows + lane;
         const bool inrow = row < (uint32_t)a.rows;
         const uint32_t n = inrow ? __ldg(a.row_symbols + row) : 0u;
         const uint32_t maxn = __reduce_max_sync(0xFFFFFFFFu, n);
         const uint64_t lo = __ldg(a.directory + tk.slice);
-        const uint32_t end = (uint32_t)(__ldg(a.directory + tk.slice + 1) - lo);
-        const GmemSrc src{a.stream + lo};
+        GmemSrc src{a.stream + lo};
         LaneState<V> st;
         st.out_pos = 0;
         if (tk.ck == 0xFFFFFFFFu) {
