@@ -14,6 +14,8 @@
 
 using namespace dtans;
 
+constexpr int kHostChunks = 8;
+
 struct dtans_dev {
     int device = 0;
     int64_t rows = 0, cols = 0, nnz = 0, nslices = 0, nwords = 0;
@@ -39,6 +41,9 @@ struct dtans_dev {
     uint32_t *d_row_map = nullptr;  // optional output row map (reordered P*A)
     uint32_t *d_order = nullptr;    // optional longest-first slice order (dynamic scheduling)
     uint64_t long_words = ~0ull;    // slices with a larger aligned window are task-decoded
+    // pipelined host path: copy-in, compute, copy-out streams and per-chunk events
+    cudaStream_t st_in = nullptr, st_comp = nullptr, st_out = nullptr;
+    cudaEvent_t ev_in[kHostChunks] = {}, ev_done[kHostChunks] = {};
 };
 
 namespace {
@@ -168,6 +173,8 @@ int configure(dtans_dev *h, const TableBlock &tb, const uint64_t *directory)
     a.nwords = h->nwords;
     a.err = h->d_err;
     a.work_counter = h->d_err + 8;
+    a.slice_lo = 0;
+    a.slice_hi = (uint32_t)h->nslices;
     int max_optin = 0, sms = 0;
     if (a.nlong) {
         h->task_smem = (int)align_up((size_t)a.table_bytes, 16);
@@ -239,10 +246,16 @@ int configure(dtans_dev *h, const TableBlock &tb, const uint64_t *directory)
 
 template <typename V>
 int launch(dtans_dev *h, const V *x, const V *y, V *out, const int64_t *row_start, int64_t *cols,
-           void *vals, bool decode_only, cudaStream_t st)
+           void *vals, bool decode_only, cudaStream_t st, int64_t s_lo = -1, int64_t s_hi = -1)
 {
     if (h->nslices == 0) return DTANS_OK;
     dev::KernelArgs a = h->base;
+    int ctas = h->ctas;
+    if (s_lo >= 0) {  // slice range (pipelined host path; static order, no long slices)
+        a.slice_lo = (uint32_t)s_lo;
+        a.slice_hi = (uint32_t)s_hi;
+        ctas = (int)std::max<int64_t>(1, std::min<int64_t>(h->ctas, (s_hi - s_lo + 31) / 32));
+    }
     if (a.dynamic) CK(cudaMemsetAsync(a.work_counter, 0, sizeof(uint32_t), st), "reset work counter");
     a.x = x;
     a.y = y;
@@ -252,11 +265,11 @@ int launch(dtans_dev *h, const V *x, const V *y, V *out, const int64_t *row_star
     a.dec_vals = vals;
     with_kernel<V>(a.dynamic != 0, [&](auto kspmv, auto kspmv0, auto kdec) -> int {
         if (decode_only)
-            kdec<<<h->ctas, h->threads, h->smem, st>>>(a);
+            kdec<<<ctas, h->threads, h->smem, st>>>(a);
         else if (y != nullptr)
-            kspmv<<<h->ctas, h->threads, h->smem, st>>>(a);
+            kspmv<<<ctas, h->threads, h->smem, st>>>(a);
         else
-            kspmv0<<<h->ctas, h->threads, h->smem, st>>>(a);
+            kspmv0<<<ctas, h->threads, h->smem, st>>>(a);
         return 0;
     });
     h->launches++;
@@ -452,6 +465,13 @@ extern "C" void dtans_free(dtans_dev *h)
     if (h->d_row_map) cudaFree(h->d_row_map);
     if (h->d_order) cudaFree(h->d_order);
     if (h->d_io) cudaFree(h->d_io);
+    for (int k = 0; k < kHostChunks; k++) {
+        if (h->ev_in[k]) cudaEventDestroy(h->ev_in[k]);
+        if (h->ev_done[k]) cudaEventDestroy(h->ev_done[k]);
+    }
+    if (h->st_in) cudaStreamDestroy(h->st_in);
+    if (h->st_comp) cudaStreamDestroy(h->st_comp);
+    if (h->st_out) cudaStreamDestroy(h->st_out);
     delete h;
 }
 
@@ -539,19 +559,48 @@ extern "C" int dtans_spmv_host(dtans_dev *h, const void *x, const void *y, void 
         h->io_bytes = need;
     }
     char *dx = (char *)h->d_io, *dy = dx + xb, *dout = dy + yb;
-    cudaStream_t st = nullptr;
-    CK(cudaMemcpyAsync(dx, x, es * (size_t)h->cols, cudaMemcpyHostToDevice, st), "H2D x");
-    if (y) CK(cudaMemcpyAsync(dy, y, es * (size_t)h->rows, cudaMemcpyHostToDevice, st), "H2D y");
-    int rc;
-    if (h->precision == 8)
-        rc = launch<double>(h, (const double *)dx, y ? (const double *)dy : nullptr, (double *)dout,
-                            nullptr, nullptr, nullptr, false, st);
-    else
-        rc = launch<float>(h, (const float *)dx, y ? (const float *)dy : nullptr, (float *)dout,
-                           nullptr, nullptr, nullptr, false, st);
-    if (rc) return rc;
-    CK(cudaMemcpyAsync(out, dout, es * (size_t)h->rows, cudaMemcpyDeviceToHost, st), "D2H out");
-    return dtans_check(h, st);
+    // Pipelined: x in, then per slice-range chunk y in (copy-in stream), the
+    // kernel on that range (compute stream) and y' out (copy-out stream), so
+    // the D2H of a chunk overlaps the H2D and decode of the next.  Containers
+    // with long slices or dynamic scheduling use one launch.
+    const bool chunked = h->base.nlong == 0 && !h->base.dynamic && h->nslices >= 64 * kHostChunks;
+    if (!h->st_in) {
+        CK(cudaStreamCreateWithFlags(&h->st_in, cudaStreamNonBlocking), "stream");
+        CK(cudaStreamCreateWithFlags(&h->st_comp, cudaStreamNonBlocking), "stream");
+        CK(cudaStreamCreateWithFlags(&h->st_out, cudaStreamNonBlocking), "stream");
+        for (int k = 0; k < kHostChunks; k++) {
+            CK(cudaEventCreateWithFlags(&h->ev_in[k], cudaEventDisableTiming), "event");
+            CK(cudaEventCreateWithFlags(&h->ev_done[k], cudaEventDisableTiming), "event");
+        }
+    }
+    const int nch = chunked ? kHostChunks : 1;
+    CK(cudaMemcpyAsync(dx, x, es * (size_t)h->cols, cudaMemcpyHostToDevice, h->st_in), "H2D x");
+    for (int k = 0; k < nch; k++) {
+        const int64_t s0 = h->nslices * k / nch, s1 = h->nslices * (k + 1) / nch;
+        const int64_t r0 = s0 * kSlice, r1 = std::min<int64_t>(s1 * kSlice, h->rows);
+        if (y && r1 > r0)
+            CK(cudaMemcpyAsync(dy + es * r0, (const char *)y + es * r0, es * (size_t)(r1 - r0),
+                               cudaMemcpyHostToDevice, h->st_in), "H2D y");
+        CK(cudaEventRecord(h->ev_in[k], h->st_in), "event");
+        CK(cudaStreamWaitEvent(h->st_comp, h->ev_in[k], 0), "wait");
+        int rc;
+        const int64_t lo = chunked ? s0 : -1, hi = chunked ? s1 : -1;
+        if (h->precision == 8)
+            rc = launch<double>(h, (const double *)dx, y ? (const double *)dy : nullptr, (double *)dout,
+                                nullptr, nullptr, nullptr, false, h->st_comp, lo, hi);
+        else
+            rc = launch<float>(h, (const float *)dx, y ? (const float *)dy : nullptr, (float *)dout,
+                               nullptr, nullptr, nullptr, false, h->st_comp, lo, hi);
+        if (rc) return rc;
+        CK(cudaEventRecord(h->ev_done[k], h->st_comp), "event");
+        CK(cudaStreamWaitEvent(h->st_out, h->ev_done[k], 0), "wait");
+        const int64_t q0 = chunked ? r0 : 0, q1 = chunked ? r1 : h->rows;
+        if (q1 > q0)
+            CK(cudaMemcpyAsync((char *)out + es * q0, dout + es * q0, es * (size_t)(q1 - q0),
+                               cudaMemcpyDeviceToHost, h->st_out), "D2H out");
+    }
+    CK(cudaStreamSynchronize(h->st_out), "synchronize");
+    return dtans_check(h, h->st_comp);
 }
 
 extern "C" int dtans_decode(dtans_dev *h, const int64_t *row_start, int64_t *cols, void *valbits,

@@ -88,6 +88,7 @@ struct KernelArgs {
     const uint32_t *row_map;      // optional: y/out index of encoded row i (row-reordered P*A)
     // work distribution
     int32_t dynamic;              // 1: atomic ticket counter instead of a static stride
+    uint32_t slice_lo, slice_hi;  // static order: slices [slice_lo, slice_hi) of this launch
     uint32_t *work_counter;       // zeroed before every dynamic launch
     const uint32_t *slice_order;  // optional: ticket -> slice (longest first)
 };
@@ -847,11 +848,11 @@ __global__ void __launch_bounds__(kThreads, 1) dtans_kernel(const KernelArgs a)
     }
     __syncthreads();
 
-    const uint32_t nsl = (uint32_t)a.nslices;
     const uint32_t rows = (uint32_t)a.rows;  // < 2^32 (checked at upload)
-    const uint32_t first = blockIdx.x * kWarps + warp;
     const uint32_t stride = gridDim.x * kWarps;
     if constexpr (!kDyn) {
+        const uint32_t nsl = a.slice_hi;
+        const uint32_t first = a.slice_lo + blockIdx.x * kWarps + warp;
         // static order: slices first, first + stride, ...
         if (lane == 0)
             for (int b = 0; b < kRing; b++) {
@@ -899,6 +900,7 @@ __global__ void __launch_bounds__(kThreads, 1) dtans_kernel(const KernelArgs a)
         }
         return;
     }
+    const uint32_t nsl = (uint32_t)a.nslices;
     // Dynamic order (skewed containers): each claim takes the next ticket of
     // a global counter, in the longest-first order of a.slice_order; tickets
     // are claimed kRing slices before they are decoded, so the atomic's
