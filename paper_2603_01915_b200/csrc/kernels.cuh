@@ -476,6 +476,51 @@ template <typename V> struct LaneState {
     int64_t out_pos;
 };
 
+// The slice's final segment: every active lane is in its last segment, so
+// no digits are folded and no checks/unconditional loads happen.  NP = pairs
+// with any valid position in the warp (compile-time, so no per-pair
+// branches); slots past them are pads that only matter if they can escape,
+// in which case the caller passes NP = 4.
+template <typename V, bool kDecode, int NP, class Src>
+__device__ __forceinline__ void final_segment(const KernelArgs &a, const Ctx &C, const V *__restrict__ x, Src &src,
+                                              const uint32_t jf, const uint32_t n, const uint32_t maxn,
+                                              LaneState<V> &st, const int lane)
+{
+    using T = ValueTraits<V>;
+    using Bits = typename T::Bits;
+    const bool act = jf < ((n + 7u) >> 3);
+    uint32_t so[8], e[8], ds[4];
+    Bits vs[4];
+    slot_offsets(st.w0, st.w1, st.w2, so);
+#pragma unroll
+    for (int p = 0; p < 4; p++) {
+        if (p < NP) {
+            lookup_pair<Bits>(C, so[2 * p], so[2 * p + 1], e[2 * p], e[2 * p + 1], ds[p], vs[p]);
+        } else {
+            e[2 * p] = e[2 * p + 1] = 0u;
+            ds[p] = 0u;
+            vs[p] = 0;
+        }
+    }
+    payload_event<T>(C, src, st.cur, act, e, ds, vs, lane);
+    const uint32_t base = 8u * jf;
+#pragma unroll
+    for (int p = 0; p < NP; p++) {
+        if (base + 2u * p < n) {
+            st.col += ds[p];
+            if (kDecode) {
+                a.dec_cols[st.out_pos] = (int64_t)st.col;
+                reinterpret_cast<Bits *>(a.dec_vals)[st.out_pos] = vs[p];
+                st.out_pos++;
+            } else {
+                const V xv = __ldg(x + min(st.col, C.cols_m1));
+                st.acc = T::add(st.acc, T::mul(T::from_bits(vs[p]), xv));
+            }
+        }
+    }
+    (void)maxn;
+}
+
 // Segments [j0, j1) of a slice (j1 <= max_nseg).  If j1 == max_nseg the
 // last one is the final segment: every active lane is in its last segment,
 // so no digits are folded and no checks/unconditional loads happen, and
@@ -512,38 +557,15 @@ __device__ __forceinline__ bool decode_range(const KernelArgs &a, const Ctx &C, 
     }
     if (j1 == max_nseg && max_nseg > 0) {
         src.advance(st.cur, lane);
+        // pairs the final segment needs: (maxn - 8 jf) / 2 (n is even); all 4
+        // lookups are needed only when pads may escape (escape-only table)
         const uint32_t jf = max_nseg - 1;
-        const bool act = jf < nseg;
-        uint32_t so[8], e[8], ds[4];
-        Bits vs[4];
-        slot_offsets(st.w0, st.w1, st.w2, so);
-        const uint32_t base = 8u * jf;
-#pragma unroll
-        for (int p = 0; p < 4; p++) {
-            if (!C.pads_ok || base + 2u * p < maxn) {  // uniform
-                lookup_pair<Bits>(C, so[2 * p], so[2 * p + 1], e[2 * p], e[2 * p + 1], ds[p], vs[p]);
-            } else {
-                e[2 * p] = e[2 * p + 1] = 0u;
-                ds[p] = 0u;
-                vs[p] = 0;
-            }
-        }
-        payload_event<T>(C, src, st.cur, act, e, ds, vs, lane);
-#pragma unroll
-        for (int p = 0; p < 4; p++) {
-            if (base + 2u * p < maxn) {  // uniform
-                if (base + 2u * p < n) {
-                    st.col += ds[p];
-                    if (kDecode) {
-                        a.dec_cols[st.out_pos] = (int64_t)st.col;
-                        reinterpret_cast<Bits *>(a.dec_vals)[st.out_pos] = vs[p];
-                        st.out_pos++;
-                    } else {
-                        const V xv = __ldg(x + min(st.col, C.cols_m1));
-                        st.acc = T::add(st.acc, T::mul(T::from_bits(vs[p]), xv));
-                    }
-                }
-            }
+        const uint32_t np = C.pads_ok ? (maxn - 8u * jf) >> 1 : 4u;
+        switch (np) {  // uniform
+        case 1: final_segment<V, kDecode, 1>(a, C, x, src, jf, n, maxn, st, lane); break;
+        case 2: final_segment<V, kDecode, 2>(a, C, x, src, jf, n, maxn, st, lane); break;
+        case 3: final_segment<V, kDecode, 3>(a, C, x, src, jf, n, maxn, st, lane); break;
+        default: final_segment<V, kDecode, 4>(a, C, x, src, jf, n, maxn, st, lane); break;
         }
     }
     return true;
