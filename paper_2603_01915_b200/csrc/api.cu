@@ -281,7 +281,7 @@ int launch(dtans_dev *h, const V *x, const V *y, V *out, const int64_t *row_star
         } else {
             if (a.ntasks) dev::dtans_task_kernel<V, false><<<h->task_ctas, 512, h->task_smem, st>>>(a);
             if (a.nsolo) dev::dtans_solo_kernel<V, false><<<h->solo_ctas, 256, h->solo_smem, st>>>(a);
-            const unsigned nb = a.nlong;
+            const unsigned nb = a.nlong_small_blocks + (a.nlong - a.nlong_small);
             if (y != nullptr)
                 dev::dtans_finalize_kernel<V, true><<<nb, 256, 0, st>>>(a);
             else
@@ -345,6 +345,11 @@ extern "C" int dtans_upload(const dtans_container_view *c, int device, dtans_dev
         h->base.ntasks = (uint32_t)li.tasks.size();
         h->base.nsolo = (uint32_t)li.solo.size();
         h->base.nlong = (uint32_t)li.slices.size();
+        uint32_t small = 0;
+        while (small < li.slices.size() && li.slices[small].nparts <= 32) small++;
+        h->base.nlong_small = small;
+        h->base.nlong_small_blocks = (small + 7) / 8;
+        h->base.single_direct = 1;
     }
 
     // one allocation: [tables][row_symbols][directory][stream + pad][err]

@@ -285,8 +285,13 @@ int build_long_index(const dtans_container_view *c, int seg_threshold, uint64_t 
                      [](const LongTask &a, const LongTask &b) { return a.j1 - a.j0 > b.j1 - b.j0; });
     std::stable_sort(out.solo.begin(), out.solo.end(),
                      [](const SoloTask &a, const SoloTask &b) { return a.j1 - a.j0 > b.j1 - b.j0; });
-    for (size_t i = 0; i < longs.size(); i++)
-        out.slices.push_back(LongSlice{longs[i], base[i], base[i + 1] - base[i], 0});
+    // finalize order: slices with <= 32 partials first (warp per slice), then
+    // the rest (CTA per slice)
+    for (int pass = 0; pass < 2; pass++)
+        for (size_t i = 0; i < longs.size(); i++) {
+            const uint32_t np = base[i + 1] - base[i];
+            if ((np <= 32) == (pass == 0)) out.slices.push_back(LongSlice{longs[i], base[i], np, 0});
+        }
     out.nparts = base.back();
     if (out.pool.empty()) out.pool.push_back(0);
     return DTANS_OK;

@@ -80,6 +80,8 @@ struct KernelArgs {
     uint32_t long_seg;            // slices with more segments go to the task kernel
     uint32_t long_words;          // ... and slices with more stream words
     uint32_t ntasks, nlong, nsolo;
+    uint32_t nlong_small, nlong_small_blocks;  // finalize: slices with <= 32 partials come first
+    int32_t single_direct;                      // single-task slices write y' in the task kernel
     const LongTask *tasks;
     const SoloTask *solo;
     const uint32_t *ck_pool;
@@ -685,7 +687,19 @@ __global__ void __launch_bounds__(512, 2) dtans_task_kernel(const KernelArgs a)
         if (kDecode && inrow) st.out_pos = __ldg(a.row_start + row) + 4ll * tk.j0;
         const bool ok = decode_range<V, kDecode>(a, C, x, src, tk.cur1, n, maxn, tk.j0, tk.j1, st, lane);
         report(a, C, ok, st.cur, tk.cur1, tk.last ? n : 0u, st.col, lane);
-        if (!kDecode) reinterpret_cast<V *>(a.partials)[(size_t)tk.part * 32 + lane] = st.acc;
+        if (!kDecode) {
+            if (tk.last && tk.j0 == 0) {
+                // the slice is this single task: y' = acc + y directly
+                if (inrow) {
+                    const uint32_t orow = a.row_map != nullptr ? __ldg(a.row_map + row) : row;
+                    V res = st.acc;
+                    if (a.y != nullptr) res = ValueTraits<V>::add(res, reinterpret_cast<const V *>(a.y)[orow]);
+                    reinterpret_cast<V *>(a.out)[orow] = res;
+                }
+            } else {
+                reinterpret_cast<V *>(a.partials)[(size_t)tk.part * 32 + lane] = st.acc;
+            }
+        }
     }
 }
 
@@ -799,18 +813,40 @@ __global__ void __launch_bounds__(256) dtans_solo_kernel(const KernelArgs a)
     }
 }
 
-// Long-slice rows: y' = (sum of the row's task partials) + y.  One CTA of
-// 8 warps per long slice: warp w adds the partials k = w, w+8, ... of all 32
-// rows (lane = row, coalesced), then the 8 warp sums are added in warp order:
-// a fixed order, so the result is deterministic.
+// Long-slice rows: y' = (sum of the row's task partials) + y, in a fixed
+// order so the result is deterministic.  Each CTA of 8 warps takes 8 slices
+// (warp = slice, lane = row) when the slices have <= 32 partials; a slice
+// with more (a long row split into many tasks) gets the whole CTA: warp w
+// adds the partials k = w, w+8, ... and the 8 warp sums are added in warp
+// order.  Slices made of a single task wrote y' directly (task kernel).
 template <typename V, bool kHasY>
 __global__ void __launch_bounds__(256) dtans_finalize_kernel(const KernelArgs a)
 {
     using T = ValueTraits<V>;
     __shared__ V red[8][32];
-    const LongSlice ls = a.longs[blockIdx.x];
     const uint32_t lane = threadIdx.x & 31u, w = threadIdx.x >> 5;
-    const V *part = reinterpret_cast<const V *>(a.partials) + (size_t)ls.part_base * 32 + lane;
+    const V *parts = reinterpret_cast<const V *>(a.partials);
+    auto finish = [&](const LongSlice &ls, V s) {
+        const uint32_t row = ls.slice * kSliceRows + lane;
+        if (row < (uint32_t)a.rows) {
+            const uint32_t orow = a.row_map != nullptr ? __ldg(a.row_map + row) : row;
+            if (kHasY) s = T::add(s, reinterpret_cast<const V *>(a.y)[orow]);
+            reinterpret_cast<V *>(a.out)[orow] = s;
+        }
+    };
+    if (blockIdx.x < a.nlong_small_blocks) {
+        const uint32_t i = blockIdx.x * 8u + w;
+        if (i >= a.nlong_small) return;
+        const LongSlice ls = a.longs[i];
+        if (ls.nparts <= 1 && a.single_direct) return;  // written by the task kernel
+        const V *part = parts + (size_t)ls.part_base * 32 + lane;
+        V acc = part[0];
+        for (uint32_t k = 1; k < ls.nparts; k++) acc = T::add(acc, part[(size_t)k * 32]);
+        finish(ls, acc);
+        return;
+    }
+    const LongSlice ls = a.longs[a.nlong_small + (blockIdx.x - a.nlong_small_blocks)];
+    const V *part = parts + (size_t)ls.part_base * 32 + lane;
     V acc = V(0);
     uint32_t k = w;
     for (; k + 24 < ls.nparts; k += 32) {
@@ -825,12 +861,7 @@ __global__ void __launch_bounds__(256) dtans_finalize_kernel(const KernelArgs a)
         V s = red[0][lane];
 #pragma unroll
         for (int q = 1; q < 8; q++) s = T::add(s, red[q][lane]);
-        const uint32_t row = ls.slice * kSliceRows + lane;
-        if (row < (uint32_t)a.rows) {
-            const uint32_t orow = a.row_map != nullptr ? __ldg(a.row_map + row) : row;
-            if (kHasY) s = T::add(s, reinterpret_cast<const V *>(a.y)[orow]);
-            reinterpret_cast<V *>(a.out)[orow] = s;
-        }
+        finish(ls, s);
     }
 }
 
