@@ -6,6 +6,7 @@
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
+#include <thread>
 #include <vector>
 
 #include "checkpoints.h"
@@ -23,6 +24,8 @@ struct dtans_dev {
     void *d_base = nullptr;     // single allocation for all container arrays
     size_t d_bytes = 0;
     uint32_t *d_tables = nullptr;
+    uint32_t *d_blob = nullptr;     // chunk blobs (kernels.cuh ChunkRec)
+    uint64_t blob_words = 0;
     uint32_t *d_row_symbols = nullptr;
     uint64_t *d_directory = nullptr;
     uint32_t *d_stream = nullptr;
@@ -39,8 +42,10 @@ struct dtans_dev {
     size_t long_bytes = 0;
     int task_ctas = 0, task_smem = 0, solo_ctas = 0, solo_smem = 0;
     uint32_t *d_row_map = nullptr;  // optional output row map (reordered P*A)
-    uint32_t *d_order = nullptr;    // optional longest-first slice order (dynamic scheduling)
-    uint64_t long_words = ~0ull;    // slices with a larger aligned window are task-decoded
+    std::vector<dev::ChunkRec> chunks;  // work list of the main kernel (host copy)
+    dev::ChunkRec *d_chunks = nullptr;
+    bool dinline = false;           // delta symbols inline in the slot table
+    int sms = 0;
     // pipelined host path: copy-in, compute, copy-out streams and per-chunk events
     cudaStream_t st_in = nullptr, st_comp = nullptr, st_out = nullptr;
     cudaEvent_t ev_in[kHostChunks] = {}, ev_done[kHostChunks] = {};
@@ -61,13 +66,21 @@ int cuda_fail(cudaError_t e, const char *what)
 
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
-// Compact slot tables: entry = digit | (base-1) << 8 | id << 16 with id the
-// index of the slot's symbol in the domain dictionary (ascending retained
-// symbols) and id = n_retained for escape slots.
+// Shared-memory table image: [dtab u32 4096][vtab u32 4096][ddict][vdict].
+// Entry = digit | (base-1) << 8 | F << 16.  Value domain: F = byte offset of
+// the symbol in the replicated value dictionary (id * rep_v * width; escapes
+// point at the dummy element nv).  Delta domain: inline (every retained
+// delta < 0xFFFF): F = the delta, 0xFFFF for escapes; otherwise F = byte
+// offset in the replicated delta dictionary.  Dictionaries hold the retained
+// symbols ascending; element e of copy c lives at (e * rep + c) * width.
 struct TableBlock {
-    std::vector<uint32_t> words;  // [dtab][vtab][ddict (+pad)][vdict (+pad)]
+    std::vector<uint32_t> tabs;                // [dtab 4096][vtab 4096]
+    std::vector<uint8_t> ddict, vdict;         // replicated dictionaries (16-byte padded)
     int32_t off_ddict = 0, off_vdict = 0;
+    int32_t rep_d = 1, rep_v = 1;
     uint32_t nd = 0, nv = 0;
+    uint32_t desc_min = 0, vesc_min = 0;
+    bool dinline = false;
 };
 
 TableBlock build_table_block(const uint8_t *recs, int precision)
@@ -112,58 +125,157 @@ TableBlock build_table_block(const uint8_t *recs, int precision)
     TableBlock tb;
     tb.nd = (uint32_t)dd.size();
     tb.nv = (uint32_t)vd.size();
-    const size_t dict_d_words = align_up(dd.size() + 1, 4);
-    const size_t vw = precision == 8 ? 2 : 1;
-    const size_t dict_v_words = align_up((vd.size() + 1) * vw, 4);
-    tb.words.assign(2 * kK + dict_d_words + dict_v_words, 0);
-    tb.off_ddict = (int32_t)(2 * kK * 4);
-    tb.off_vdict = (int32_t)((2 * kK + dict_d_words) * 4);
+    tb.dinline = dd.empty() || dd.back() < 0xFFFFull;
+    const char *ei = getenv("DTANS_DINLINE");
+    if (ei && atoi(ei) == 0) tb.dinline = false;
+    const uint32_t vw = (uint32_t)precision;  // value width in bytes
+    // replication: conflict-free dictionary reads need 32 lanes x width
+    // bytes = all 32 banks per wavefront; keep F < 2^16 and each dictionary
+    // within a shared-memory budget
+    auto pick_rep = [](uint32_t n_el, uint32_t w, uint32_t rmax, uint32_t budget) {
+        uint32_t r = rmax;
+        while (r > 1 && ((uint64_t)(n_el + 1) * r * w > 65536u || (uint64_t)(n_el + 1) * r * w > budget)) r >>= 1;
+        return r;
+    };
+    const char *er = getenv("DTANS_REP");
+    const uint32_t rcap = er ? (uint32_t)std::max(1, atoi(er)) : 32u;
+    tb.rep_v = (int32_t)pick_rep(tb.nv, vw, std::min<uint32_t>(rcap, 128u / vw), 36u * 1024u);
+    tb.rep_d = tb.dinline ? 1 : (int32_t)pick_rep(tb.nd, 4, std::min<uint32_t>(rcap, 32u), 8u * 1024u);
+    const size_t dict_d_bytes = tb.dinline ? 0 : align_up((size_t)(tb.nd + 1) * tb.rep_d * 4, 16);
+    const size_t dict_v_bytes = align_up((size_t)(tb.nv + 1) * tb.rep_v * vw, 16);
+    tb.tabs.assign(2 * kK, 0);
+    tb.ddict.assign(dict_d_bytes, 0);
+    tb.vdict.assign(dict_v_bytes, 0);
     for (int j = 0; j < kK; j++) {
-        // id field = byte offset of the symbol in its dictionary; escapes
-        // point at the dummy slot after the retained symbols
-        const uint32_t did = 4u * (desc[j] ? tb.nd
-                                           : (uint32_t)(std::lower_bound(dd.begin(), dd.end(), dsym[j]) - dd.begin()));
-        const uint32_t vid = (uint32_t)(4 * vw) *
-                             (vesc[j] ? tb.nv
-                                      : (uint32_t)(std::lower_bound(vd.begin(), vd.end(), vsym[j]) - vd.begin()));
-        tb.words[j] = (uint32_t)ddig[j] | ((uint32_t)dbm1[j] << 8) | (did << 16);
-        tb.words[kK + j] = (uint32_t)vdig[j] | ((uint32_t)vbm1[j] << 8) | (vid << 16);
+        uint32_t fd;
+        if (tb.dinline)
+            fd = desc[j] ? 0xFFFFu : (uint32_t)dsym[j];
+        else
+            fd = 4u * (uint32_t)tb.rep_d *
+                 (desc[j] ? tb.nd : (uint32_t)(std::lower_bound(dd.begin(), dd.end(), dsym[j]) - dd.begin()));
+        const uint32_t fv = vw * (uint32_t)tb.rep_v *
+                            (vesc[j] ? tb.nv : (uint32_t)(std::lower_bound(vd.begin(), vd.end(), vsym[j]) - vd.begin()));
+        tb.tabs[j] = (uint32_t)ddig[j] | ((uint32_t)dbm1[j] << 8) | (fd << 16);
+        tb.tabs[kK + j] = (uint32_t)vdig[j] | ((uint32_t)vbm1[j] << 8) | (fv << 16);
     }
-    for (size_t i = 0; i < dd.size(); i++) tb.words[2 * kK + i] = (uint32_t)dd[i];
-    uint32_t *vdw = tb.words.data() + 2 * kK + dict_d_words;
-    for (size_t i = 0; i < vd.size(); i++) {
-        if (vw == 2) {
-            vdw[2 * i] = (uint32_t)vd[i];
-            vdw[2 * i + 1] = (uint32_t)(vd[i] >> 32);
-        } else {
-            vdw[i] = (uint32_t)vd[i];
+    tb.desc_min = tb.dinline ? dev::kDeltaInlineEsc : (4u * (uint32_t)tb.rep_d * tb.nd) << 16;
+    tb.vesc_min = (vw * (uint32_t)tb.rep_v * tb.nv) << 16;
+    if (!tb.dinline)
+        for (size_t e = 0; e < dd.size(); e++)
+            for (int c = 0; c < tb.rep_d; c++) {
+                const uint32_t v = (uint32_t)dd[e];
+                memcpy(tb.ddict.data() + (e * tb.rep_d + c) * 4, &v, 4);
+            }
+    for (size_t e = 0; e < vd.size(); e++)
+        for (int c = 0; c < tb.rep_v; c++) {
+            if (vw == 8)
+                memcpy(tb.vdict.data() + (e * tb.rep_v + c) * 8, &vd[e], 8);
+            else {
+                const uint32_t v = (uint32_t)vd[e];
+                memcpy(tb.vdict.data() + (e * tb.rep_v + c) * 4, &v, 4);
+            }
         }
-    }
     return tb;
 }
 
-// Dispatch on the compile-time CTA size.
-template <typename V, class F>
-int with_kernel(bool dyn, F &&f)
+// Shared-memory plan (dynamic smem offsets; the dynamic window starts at
+// shared address 0x400 mod 16 KB on sm_90+/sm_100, which the kernels check):
+//   [bars][metas][warp ctl][low dictionaries]   below kTabOff
+//   [delta slot table][value slot table]         at kTabOff (16 KB aligned address)
+//   [other dictionaries][staging rings][overrun slack]
+// The global table image mirrors [off_img, end of dictionaries).
+constexpr int32_t kTabOff = 0x3C00;
+struct SmemPlan {
+    int32_t off_bars = 0, off_meta = 0, off_ctl = 0, off_bufs = 0, bufb = 0, nring = 3, total = 0;
+    int32_t off_img = 0, off_tab = kTabOff, off_ddict = 0, off_vdict = 0;
+    std::vector<uint32_t> image;
+};
+
+SmemPlan plan_smem(const TableBlock &tb, int max_optin, int nring)
 {
-    if (dyn)
-        return f(dev::dtans_kernel<V, false, true, true, 1024>, dev::dtans_kernel<V, false, false, true, 1024>,
-                 dev::dtans_kernel<V, true, false, true, 1024>);
-    return f(dev::dtans_kernel<V, false, true, false, 1024>, dev::dtans_kernel<V, false, false, false, 1024>,
-             dev::dtans_kernel<V, true, false, false, 1024>);
+    SmemPlan p;
+    p.off_bars = 0;
+    p.off_meta = dev::kMaxWarps * dev::kMaxRing * 8;
+    p.off_ctl = 2 * dev::kMaxWarps * dev::kMaxRing * 8;
+    size_t low = (size_t)p.off_ctl + dev::kMaxWarps * 32;
+    const size_t low0 = low;
+    size_t high = (size_t)kTabOff + dev::kTabBytes;
+    auto place = [&](size_t bytes) -> int32_t {
+        if (bytes == 0) return (int32_t)low;
+        if (low + bytes <= (size_t)kTabOff) {
+            low += bytes;
+            return (int32_t)(low - bytes);
+        }
+        high += bytes;
+        return (int32_t)(high - bytes);
+    };
+    // the larger dictionary first gets the free space below the tables
+    if (tb.vdict.size() >= tb.ddict.size()) {
+        p.off_vdict = place(tb.vdict.size());
+        p.off_ddict = place(tb.ddict.size());
+    } else {
+        p.off_ddict = place(tb.ddict.size());
+        p.off_vdict = place(tb.vdict.size());
+    }
+    p.off_img = low > low0 ? (int32_t)low0 : kTabOff;
+    p.image.assign((high - (size_t)p.off_img) / 4, 0);
+    uint8_t *img = reinterpret_cast<uint8_t *>(p.image.data());
+    memcpy(img + (kTabOff - p.off_img), tb.tabs.data(), dev::kTabBytes);
+    if (!tb.ddict.empty()) memcpy(img + (p.off_ddict - p.off_img), tb.ddict.data(), tb.ddict.size());
+    memcpy(img + (p.off_vdict - p.off_img), tb.vdict.data(), tb.vdict.size());
+    const size_t off = align_up(high, 128);
+    p.off_bufs = (int32_t)off;
+    const int64_t avail = (int64_t)max_optin - (int64_t)off - dev::kOverrunWords * 4;
+    p.nring = nring;
+    p.bufb = (int32_t)std::max<int64_t>(0, avail / (dev::kMaxWarps * nring) / 16 * 16);
+    p.total = (int32_t)(off + (size_t)dev::kMaxWarps * nring * p.bufb + dev::kOverrunWords * 4);
+    return p;
+}
+
+// words of the blob of a chunk of slices [s0, s0+k) (kernels.cuh ChunkRec)
+uint64_t chunk_words(const uint64_t *dir, int64_t s0, int64_t k)
+{
+    return dev::chunk_hdr_words((uint32_t)k) + (uint64_t)k * 32 + ((dir[s0 + k] - dir[s0] + 3) & ~3ull);
+}
+uint64_t chunk_bytes(const uint64_t *dir, int64_t s0, int64_t k) { return 4 * chunk_words(dir, s0, k); }
+
+// Dispatch on the delta-dictionary mode.
+template <typename V, class F>
+int with_kernel(bool dinline, F &&f)
+{
+    if (dinline)
+        return f(dev::dtans_kernel<V, false, true, true>, dev::dtans_kernel<V, false, false, true>,
+                 dev::dtans_kernel<V, true, false, true>);
+    return f(dev::dtans_kernel<V, false, true, false>, dev::dtans_kernel<V, false, false, false>,
+             dev::dtans_kernel<V, true, false, false>);
+}
+
+template <typename V, class F>
+int with_long_kernels(bool dinline, F &&f)
+{
+    if (dinline)
+        return f(dev::dtans_task_kernel<V, false, true>, dev::dtans_task_kernel<V, true, true>,
+                 dev::dtans_solo_kernel<V, false, true>, dev::dtans_solo_kernel<V, true, true>);
+    return f(dev::dtans_task_kernel<V, false, false>, dev::dtans_task_kernel<V, true, false>,
+             dev::dtans_solo_kernel<V, false, false>, dev::dtans_solo_kernel<V, true, false>);
 }
 
 template <typename V>
-int configure(dtans_dev *h, const TableBlock &tb, const uint64_t *directory)
+int configure(dtans_dev *h, const TableBlock &tb, const SmemPlan &sp)
 {
     dev::KernelArgs &a = h->base;
     a.tables = h->d_tables;
-    a.table_bytes = (int32_t)(tb.words.size() * 4);
-    a.off_ddict = tb.off_ddict;
-    a.off_vdict = tb.off_vdict;
-    a.desc_min = (4u * tb.nd) << 16;
-    a.vesc_min = ((uint32_t)(sizeof(V)) * tb.nv) << 16;
+    a.table_bytes = (int32_t)(sp.image.size() * 4);
+    a.off_img = sp.off_img;
+    a.off_tab = sp.off_tab;
+    a.off_ddict = sp.off_ddict;
+    a.off_vdict = sp.off_vdict;
+    a.rep_d = tb.rep_d;
+    a.rep_v = tb.rep_v;
+    a.desc_min = tb.desc_min;
+    a.vesc_min = tb.vesc_min;
     a.pads_ok = tb.nd > 0 && tb.nv > 0;
+    a.blob = h->d_blob;
     a.row_symbols = h->d_row_symbols;
     a.directory = h->d_directory;
     a.stream = h->d_stream;
@@ -173,64 +285,43 @@ int configure(dtans_dev *h, const TableBlock &tb, const uint64_t *directory)
     a.nwords = h->nwords;
     a.err = h->d_err;
     a.work_counter = h->d_err + 8;
-    a.slice_lo = 0;
-    a.slice_hi = (uint32_t)h->nslices;
-    int max_optin = 0, sms = 0;
+    a.off_bars = sp.off_bars;
+    a.off_meta = sp.off_meta;
+    a.off_ctl = sp.off_ctl;
+    a.off_bufs = sp.off_bufs;
+    a.bufb = sp.bufb;
+    a.nring = sp.nring;
+    a.chunks = h->d_chunks;
+    a.chunk_lo = 0;
+    a.chunk_hi = (uint32_t)h->chunks.size();
+    h->dinline = tb.dinline;
+    int sms = 0;
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device), "sm count");
+    h->sms = sms;
     if (a.nlong) {
-        h->task_smem = (int)align_up((size_t)a.table_bytes, 16);
-        h->solo_smem = (int)align_up((size_t)a.table_bytes, 16);
-        CK(cudaFuncSetAttribute(dev::dtans_solo_kernel<V, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                h->solo_smem), "cudaFuncSetAttribute");
-        CK(cudaFuncSetAttribute(dev::dtans_solo_kernel<V, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                h->solo_smem), "cudaFuncSetAttribute");
-        CK(cudaFuncSetAttribute(dev::dtans_task_kernel<V, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                h->task_smem), "cudaFuncSetAttribute");
-        CK(cudaFuncSetAttribute(dev::dtans_task_kernel<V, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                h->task_smem), "cudaFuncSetAttribute");
-        int per = 0, nsm = 0;
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, dev::dtans_task_kernel<V, false>, 512, h->task_smem),
-           "occupancy");
-        CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, h->device), "sm count");
-        h->task_ctas = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)nsm * std::max(per, 1),
+        h->task_smem = (int)align_up((size_t)(a.off_img + a.table_bytes), 16);
+        h->solo_smem = h->task_smem;
+        int per = 0, pers = 0;
+        int rc = with_long_kernels<V>(tb.dinline, [&](auto kt, auto ktd, auto ks, auto ksd) -> int {
+            CK(cudaFuncSetAttribute(kt, cudaFuncAttributeMaxDynamicSharedMemorySize, h->task_smem), "attr");
+            CK(cudaFuncSetAttribute(ktd, cudaFuncAttributeMaxDynamicSharedMemorySize, h->task_smem), "attr");
+            CK(cudaFuncSetAttribute(ks, cudaFuncAttributeMaxDynamicSharedMemorySize, h->solo_smem), "attr");
+            CK(cudaFuncSetAttribute(ksd, cudaFuncAttributeMaxDynamicSharedMemorySize, h->solo_smem), "attr");
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kt, 512, h->task_smem), "occupancy");
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pers, ks, 256, h->solo_smem), "occupancy");
+            return DTANS_OK;
+        });
+        if (rc) return rc;
+        h->task_ctas = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)sms * std::max(per, 1),
                                                                     ((int64_t)a.ntasks + 15) / 16));
-        int pers = 0;
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pers, dev::dtans_solo_kernel<V, false>, 256, h->solo_smem),
-           "occupancy");
-        h->solo_ctas = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)nsm * std::max(pers, 1),
+        h->solo_ctas = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)sms * std::max(pers, 1),
                                                                     ((int64_t)a.nsolo + 255) / 256));
     }
-    CK(cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->device), "attr");
-    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device), "sm count");
-    size_t off = (size_t)a.table_bytes;
-    off = align_up(off, 16);
-    a.off_bars = (int32_t)off;
-    off += dev::kMaxWarps * dev::kRing * 8;
-    off = align_up(off, 16);
-    a.off_meta = (int32_t)off;
-    off += dev::kMaxWarps * dev::kRing * sizeof(dev::SliceMeta);
-    off = align_up(off, 128);
-    a.off_bufs = (int32_t)off;
-    // ring buffer size: the largest 16-byte-aligned slice window, capped by
-    // what fits; bigger slices are decoded straight from global memory.
-    uint64_t max_words = 4;
-    for (int64_t s = 0; s < h->nslices; s++) {
-        const uint64_t lo = directory[s] & ~3ull, hi = (directory[s + 1] + 3) & ~3ull;
-        if (hi - lo <= h->long_words) max_words = std::max<uint64_t>(max_words, hi - lo);
-    }
-    h->threads = 1024;
-    const int warps = h->threads / 32;
-    const int64_t budget =
-        ((int64_t)max_optin - (int64_t)off - dev::kOverrunWords * 4) / (warps * dev::kRing * 4);
-    if (budget < 4) return fail(DTANS_E_CUDA, "coding tables leave no shared memory for staging");
-    a.bufw = (int32_t)std::min<int64_t>((int64_t)align_up(max_words, 4), budget / 4 * 4);
-    h->staged_slices = 0;
-    for (int64_t s = 0; s < h->nslices; s++) {
-        const uint64_t lo = directory[s] & ~3ull, hi = (directory[s + 1] + 3) & ~3ull;
-        if (hi - lo <= (uint64_t)a.bufw) h->staged_slices++;
-    }
-    h->smem = (int)(off + ((size_t)warps * dev::kRing * a.bufw + dev::kOverrunWords) * 4);
+    h->threads = dev::kMaxWarps * 32;
+    h->smem = sp.total;
+    h->ctas = (int)std::max<int64_t>(1, std::min<int64_t>(sms, ((int64_t)h->chunks.size() + dev::kMaxWarps - 1) / dev::kMaxWarps));
     int per_sm = 0;
-    int rc = with_kernel<V>(h->base.dynamic != 0, [&](auto kspmv, auto kspmv0, auto kdec) -> int {
+    int rc = with_kernel<V>(tb.dinline, [&](auto kspmv, auto kspmv0, auto kdec) -> int {
         CK(cudaFuncSetAttribute(kspmv, cudaFuncAttributeMaxDynamicSharedMemorySize, h->smem), "cudaFuncSetAttribute");
         CK(cudaFuncSetAttribute(kspmv0, cudaFuncAttributeMaxDynamicSharedMemorySize, h->smem), "cudaFuncSetAttribute");
         CK(cudaFuncSetAttribute(kdec, cudaFuncAttributeMaxDynamicSharedMemorySize, h->smem), "cudaFuncSetAttribute");
@@ -239,23 +330,21 @@ int configure(dtans_dev *h, const TableBlock &tb, const uint64_t *directory)
     });
     if (rc) return rc;
     if (per_sm < 1) return fail(DTANS_E_CUDA, "kernel does not fit on an SM");
-    const int64_t ctas_needed = (h->nslices + warps - 1) / warps;
-    h->ctas = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)sms * per_sm, ctas_needed));
     return DTANS_OK;
 }
 
 template <typename V>
 int launch(dtans_dev *h, const V *x, const V *y, V *out, const int64_t *row_start, int64_t *cols,
-           void *vals, bool decode_only, cudaStream_t st, int64_t s_lo = -1, int64_t s_hi = -1)
+           void *vals, bool decode_only, cudaStream_t st, int64_t c_lo = -1, int64_t c_hi = -1)
 {
     if (h->nslices == 0) return DTANS_OK;
     dev::KernelArgs a = h->base;
-    int ctas = h->ctas;
-    if (s_lo >= 0) {  // slice range (pipelined host path; static order, no long slices)
-        a.slice_lo = (uint32_t)s_lo;
-        a.slice_hi = (uint32_t)s_hi;
-        ctas = (int)std::max<int64_t>(1, std::min<int64_t>(h->ctas, (s_hi - s_lo + 31) / 32));
+    if (c_lo >= 0) {  // chunk range (pipelined host path; static order, no long slices)
+        a.chunk_lo = (uint32_t)c_lo;
+        a.chunk_hi = (uint32_t)c_hi;
     }
+    const int64_t nch = (int64_t)a.chunk_hi - (int64_t)a.chunk_lo;
+    const int ctas = (int)std::max<int64_t>(1, std::min<int64_t>(h->sms, (nch + dev::kMaxWarps - 1) / dev::kMaxWarps));
     if (a.dynamic) CK(cudaMemsetAsync(a.work_counter, 0, sizeof(uint32_t), st), "reset work counter");
     a.x = x;
     a.y = y;
@@ -263,30 +352,37 @@ int launch(dtans_dev *h, const V *x, const V *y, V *out, const int64_t *row_star
     a.row_start = row_start;
     a.dec_cols = cols;
     a.dec_vals = vals;
-    with_kernel<V>(a.dynamic != 0, [&](auto kspmv, auto kspmv0, auto kdec) -> int {
-        if (decode_only)
-            kdec<<<ctas, h->threads, h->smem, st>>>(a);
-        else if (y != nullptr)
-            kspmv<<<ctas, h->threads, h->smem, st>>>(a);
-        else
-            kspmv0<<<ctas, h->threads, h->smem, st>>>(a);
-        return 0;
-    });
-    h->launches++;
-    if (a.nlong) {
-        if (decode_only) {
-            if (a.ntasks) dev::dtans_task_kernel<V, true><<<h->task_ctas, 512, h->task_smem, st>>>(a);
-            if (a.nsolo) dev::dtans_solo_kernel<V, true><<<h->solo_ctas, 256, h->solo_smem, st>>>(a);
-            h->launches += (a.ntasks ? 1 : 0) + (a.nsolo ? 1 : 0);
-        } else {
-            if (a.ntasks) dev::dtans_task_kernel<V, false><<<h->task_ctas, 512, h->task_smem, st>>>(a);
-            if (a.nsolo) dev::dtans_solo_kernel<V, false><<<h->solo_ctas, 256, h->solo_smem, st>>>(a);
+    if (nch > 0) {
+        with_kernel<V>(h->dinline, [&](auto kspmv, auto kspmv0, auto kdec) -> int {
+            if (decode_only)
+                kdec<<<ctas, h->threads, h->smem, st>>>(a);
+            else if (y != nullptr)
+                kspmv<<<ctas, h->threads, h->smem, st>>>(a);
+            else
+                kspmv0<<<ctas, h->threads, h->smem, st>>>(a);
+            return 0;
+        });
+        h->launches++;
+    }
+    if (a.nlong && c_lo < 0) {
+        with_long_kernels<V>(h->dinline, [&](auto kt, auto ktd, auto ks, auto ksd) -> int {
+            if (decode_only) {
+                if (a.ntasks) ktd<<<h->task_ctas, 512, h->task_smem, st>>>(a);
+                if (a.nsolo) ksd<<<h->solo_ctas, 256, h->solo_smem, st>>>(a);
+            } else {
+                if (a.ntasks) kt<<<h->task_ctas, 512, h->task_smem, st>>>(a);
+                if (a.nsolo) ks<<<h->solo_ctas, 256, h->solo_smem, st>>>(a);
+            }
+            return 0;
+        });
+        h->launches += (a.ntasks ? 1 : 0) + (a.nsolo ? 1 : 0);
+        if (!decode_only) {
             const unsigned nb = a.nlong_small_blocks + (a.nlong - a.nlong_small);
             if (y != nullptr)
                 dev::dtans_finalize_kernel<V, true><<<nb, 256, 0, st>>>(a);
             else
                 dev::dtans_finalize_kernel<V, false><<<nb, 256, 0, st>>>(a);
-            h->launches += (a.ntasks ? 1 : 0) + (a.nsolo ? 1 : 0) + 1;
+            h->launches += 1;
         }
     }
     CK(cudaGetLastError(), "kernel launch");
@@ -312,6 +408,11 @@ extern "C" int dtans_upload(const dtans_container_view *c, int device, dtans_dev
     if (c->nslices != nsl) return fail(DTANS_E_PARAM, "nslices does not match rows");
     if ((int64_t)c->directory[nsl] != c->nwords)
         return fail(DTANS_E_CORRUPT, "directory does not span the stream");
+    for (int64_t s = 0; s < nsl; s++)
+        if (c->directory[s + 1] < c->directory[s]) return fail(DTANS_E_CORRUPT, "directory is not monotone");
+    int max_optin = 0, sms = 0;
+    CK(cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device), "attr");
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device), "sm count");
 
     dtans_dev *h = new dtans_dev();
     h->device = device;
@@ -322,26 +423,37 @@ extern "C" int dtans_upload(const dtans_container_view *c, int device, dtans_dev
     h->nwords = c->nwords;
     h->precision = c->precision;
     const TableBlock tb = build_table_block(c->tables, c->precision);
+
+    // per-slice cost (segments of the longest row) and the long-slice split
+    const char *e1 = getenv("DTANS_LONG_SEG"), *e2 = getenv("DTANS_CHUNK");
+    const int long_seg = e1 ? atoi(e1) : 64, chunk = e2 ? atoi(e2) : 32;
+    std::vector<uint32_t> cost((size_t)nsl);
+    for (int64_t s = 0; s < nsl; s++) {
+        uint32_t m = 0;
+        for (int64_t i = s * kSlice; i < std::min<int64_t>((s + 1) * kSlice, c->rows); i++)
+            m = std::max(m, c->row_symbols[i]);
+        cost[s] = (m + 7) / 8;
+    }
+    // staging ring: 3 buffers per warp unless the largest (non-long) slice
+    // only fits with 2
+    uint64_t max_single = 0;
+    for (int64_t s = 0; s < nsl; s++)
+        if (cost[s] <= (uint32_t)long_seg) max_single = std::max(max_single, chunk_bytes(c->directory, s, 1));
+    SmemPlan sp = plan_smem(tb, max_optin, 3);
+    const char *er = getenv("DTANS_RING");
+    if (er ? atoi(er) == 2 : max_single > (uint64_t)sp.bufb) sp = plan_smem(tb, max_optin, 2);
+    if (sp.bufb < 512) {
+        delete h;
+        return fail(DTANS_E_CUDA, "coding tables leave no shared memory for staging");
+    }
     LongIndex li;
     {
-        const char *e1 = getenv("DTANS_LONG_SEG"), *e2 = getenv("DTANS_CHUNK");
-        const int long_seg = e1 ? atoi(e1) : 64, chunk = e2 ? atoi(e2) : 32;
-        // slices whose stream window cannot be staged in a ring buffer go to
-        // the task kernels as well (their words would be read uncached)
-        int max_optin = 0;
-        if (cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device) != cudaSuccess)
-            max_optin = 227 * 1024;
-        const int64_t fixed = (int64_t)tb.words.size() * 4 + dev::kMaxWarps * dev::kRing * (8 + sizeof(dev::SliceMeta)) +
-                              256 + dev::kOverrunWords * 4;
-        const uint64_t max_words = (uint64_t)std::max<int64_t>(4, (max_optin - fixed) / (dev::kMaxWarps * dev::kRing * 4) / 4 * 4);
+        const uint64_t max_words = (uint64_t)(sp.bufb - 16 - 128) / 4;
         const int rc0 = build_long_index(c, long_seg, max_words, std::max(1, chunk), li);
         if (rc0) {
             delete h;
             return rc0;
         }
-        h->base.long_seg = li.slices.empty() ? 0xFFFFFFFFu : (uint32_t)long_seg;
-        h->long_words = max_words;
-        h->base.long_words = li.slices.empty() ? 0xFFFFFFFFu : (uint32_t)std::min<uint64_t>(max_words, 0xFFFFFFFEull);
         h->base.ntasks = (uint32_t)li.tasks.size();
         h->base.nsolo = (uint32_t)li.solo.size();
         h->base.nlong = (uint32_t)li.slices.size();
@@ -351,14 +463,73 @@ extern "C" int dtans_upload(const dtans_container_view *c, int device, dtans_dev
         h->base.nlong_small_blocks = (small + 7) / 8;
         h->base.single_direct = 1;
     }
+    // chunk list over the slices the main kernel decodes
+    {
+        std::vector<uint8_t> is_long((size_t)nsl, 0);
+        for (const LongSlice &ls : li.slices) is_long[ls.slice] = 1;
+        double mean = 0;
+        uint32_t mx = 0;
+        for (int64_t s = 0; s < nsl; s++) {
+            const uint32_t cs = is_long[s] ? 0 : cost[s];
+            mean += cs;
+            mx = std::max(mx, cs);
+        }
+        mean /= (double)std::max<int64_t>(nsl, 1);
+        const char *ed = getenv("DTANS_DYNAMIC");
+        const bool dyn = ed ? atoi(ed) != 0 : (mx > 4.0 * std::max(mean, 1.0));
+        h->base.dynamic = dyn ? 1 : 0;
+        bool sorted = true;
+        for (int64_t s = 1; s < nsl && sorted; s++)
+            sorted = (is_long[s] ? 0 : cost[s]) <= (is_long[s - 1] ? 0 : cost[s - 1]);
+        const char *ek = getenv("DTANS_KCHUNK");
+        const int64_t kcap = ek ? std::max(1, std::min(atoi(ek), dev::kMaxChunk))
+                                : std::max<int64_t>(1, std::min<int64_t>(dev::kMaxChunk,
+                                                                          nsl / ((int64_t)sms * dev::kMaxWarps * 4)));
+        uint64_t blob_words = 0;
+        auto push = [&](int64_t s0, int64_t k) {
+            const uint64_t w = chunk_words(c->directory, s0, k);
+            h->chunks.push_back(dev::ChunkRec{blob_words, (uint32_t)s0, (uint32_t)k | (uint32_t)w << 8});
+            blob_words += w;
+        };
+        if (dyn && !sorted) {
+            // skewed, unsorted: single-slice chunks, longest first
+            std::vector<uint32_t> order;
+            for (int64_t s = 0; s < nsl; s++)
+                if (!is_long[s]) order.push_back((uint32_t)s);
+            std::stable_sort(order.begin(), order.end(), [&](uint32_t p, uint32_t q) { return cost[p] > cost[q]; });
+            for (uint32_t s : order) push(s, 1);
+        } else {
+            int64_t s = 0;
+            while (s < nsl) {
+                if (is_long[s]) {
+                    s++;
+                    continue;
+                }
+                int64_t k = 1;
+                while (k < kcap && s + k < nsl && !is_long[s + k] &&
+                       chunk_bytes(c->directory, s, k + 1) <= (uint64_t)sp.bufb)
+                    k++;
+                push(s, k);
+                s += k;
+            }
+        }
+        h->blob_words = blob_words;
+    }
 
-    // one allocation: [tables][row_symbols][directory][stream + pad][err]
+    // one allocation: [table image][chunk blobs][err][chunk records]
+    //   + [row_symbols][directory][stream + pad] when long slices need them
+    const bool need_raw = !li.slices.empty();
     size_t off = 0;
-    const size_t o_tb = off; off = align_up(off + tb.words.size() * 4, 256);
-    const size_t o_rs = off; off = align_up(off + sizeof(uint32_t) * (size_t)std::max<int64_t>(c->rows, 1), 256);
-    const size_t o_di = off; off = align_up(off + sizeof(uint64_t) * (size_t)(nsl + 1), 256);
-    const size_t o_st = off; off = align_up(off + sizeof(uint32_t) * ((size_t)c->nwords + dev::kStreamPadWords), 256);
+    const size_t o_tb = off; off = align_up(off + sp.image.size() * 4, 256);
+    const size_t o_bl = off; off = align_up(off + sizeof(uint32_t) * (size_t)std::max<uint64_t>(h->blob_words, 4), 256);
     const size_t o_er = off; off = align_up(off + 64, 256);
+    const size_t o_ch = off; off = align_up(off + sizeof(dev::ChunkRec) * std::max<size_t>(h->chunks.size(), 1), 256);
+    size_t o_rs = 0, o_di = 0, o_st = 0;
+    if (need_raw) {
+        o_rs = off; off = align_up(off + sizeof(uint32_t) * (size_t)std::max<int64_t>(c->rows, 1), 256);
+        o_di = off; off = align_up(off + sizeof(uint64_t) * (size_t)(nsl + 1), 256);
+        o_st = off; off = align_up(off + sizeof(uint32_t) * ((size_t)c->nwords + dev::kStreamPadWords), 256);
+    }
     cudaError_t e = cudaMalloc(&h->d_base, off);
     if (e != cudaSuccess) {
         delete h;
@@ -367,10 +538,14 @@ extern "C" int dtans_upload(const dtans_container_view *c, int device, dtans_dev
     h->d_bytes = off;
     char *b = (char *)h->d_base;
     h->d_tables = (uint32_t *)(b + o_tb);
-    h->d_row_symbols = (uint32_t *)(b + o_rs);
-    h->d_directory = (uint64_t *)(b + o_di);
-    h->d_stream = (uint32_t *)(b + o_st);
+    h->d_blob = (uint32_t *)(b + o_bl);
     h->d_err = (unsigned int *)(b + o_er);
+    h->d_chunks = (dev::ChunkRec *)(b + o_ch);
+    if (need_raw) {
+        h->d_row_symbols = (uint32_t *)(b + o_rs);
+        h->d_directory = (uint64_t *)(b + o_di);
+        h->d_stream = (uint32_t *)(b + o_st);
+    }
     int rc = DTANS_OK;
     auto cp = [&](void *dst, const void *src, size_t n) {
         if (rc == DTANS_OK && n) {
@@ -378,15 +553,45 @@ extern "C" int dtans_upload(const dtans_container_view *c, int device, dtans_dev
             if (ce != cudaSuccess) rc = cuda_fail(ce, "upload");
         }
     };
-    cp(h->d_tables, tb.words.data(), tb.words.size() * 4);
-    cp(h->d_row_symbols, c->row_symbols, sizeof(uint32_t) * (size_t)c->rows);
-    cp(h->d_directory, c->directory, sizeof(uint64_t) * (size_t)(nsl + 1));
-    cp(h->d_stream, c->stream, sizeof(uint32_t) * (size_t)c->nwords);
-    if (rc == DTANS_OK) {
-        cudaError_t ce = cudaMemset(h->d_stream + c->nwords, 0, sizeof(uint32_t) * dev::kStreamPadWords);
-        if (ce == cudaSuccess) ce = cudaMemset(h->d_err, 0, 64);
-        if (ce != cudaSuccess) rc = cuda_fail(ce, "memset");
+    auto zero = [&](void *dst, size_t n) {
+        if (rc == DTANS_OK && n) {
+            cudaError_t ce = cudaMemset(dst, 0, n);
+            if (ce != cudaSuccess) rc = cuda_fail(ce, "memset");
+        }
+    };
+    cp(h->d_tables, sp.image.data(), sp.image.size() * 4);
+    {
+        // assemble the chunk blobs on the host (multithreaded) and upload
+        std::vector<uint32_t> blob((size_t)h->blob_words, 0u);
+        const size_t nch = h->chunks.size();
+        const unsigned nt = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+        std::vector<std::thread> th;
+        for (unsigned t = 0; t < nt; t++)
+            th.emplace_back([&, t]() {
+                for (size_t q = nch * t / nt; q < nch * (t + 1) / nt; q++) {
+                    const dev::ChunkRec &r = h->chunks[q];
+                    const int64_t s0 = r.s0, k = r.kw & 0xFF;
+                    uint32_t *p = blob.data() + r.off;
+                    const uint64_t base = c->directory[s0];
+                    for (int64_t i = 0; i <= k; i++) p[i] = (uint32_t)(c->directory[s0 + i] - base);
+                    p += dev::chunk_hdr_words((uint32_t)k);
+                    const int64_t r0 = s0 * kSlice, r1 = std::min<int64_t>((s0 + k) * kSlice, c->rows);
+                    memcpy(p, c->row_symbols + r0, sizeof(uint32_t) * (size_t)(r1 - r0));
+                    p += k * 32;
+                    memcpy(p, c->stream + base, sizeof(uint32_t) * (size_t)(c->directory[s0 + k] - base));
+                }
+            });
+        for (auto &t : th) t.join();
+        cp(h->d_blob, blob.data(), blob.size() * 4);
     }
+    if (need_raw) {
+        cp(h->d_row_symbols, c->row_symbols, sizeof(uint32_t) * (size_t)c->rows);
+        cp(h->d_directory, c->directory, sizeof(uint64_t) * (size_t)(nsl + 1));
+        cp(h->d_stream, c->stream, sizeof(uint32_t) * (size_t)c->nwords);
+        zero(h->d_stream + c->nwords, sizeof(uint32_t) * dev::kStreamPadWords);
+    }
+    zero(h->d_err, 64);
+    cp(h->d_chunks, h->chunks.data(), sizeof(dev::ChunkRec) * h->chunks.size());
     if (rc == DTANS_OK && !li.slices.empty()) {
         const size_t tb_b = align_up(li.tasks.size() * sizeof(LongTask), 256) +
                             align_up(li.solo.size() * sizeof(SoloTask), 256);
@@ -406,54 +611,17 @@ extern "C" int dtans_upload(const dtans_container_view *c, int device, dtans_dev
             h->base.partials = lb + tb_b + pl_b + ls_b;
             cp(lb, li.tasks.data(), li.tasks.size() * sizeof(LongTask));
             cp((void *)h->base.solo, li.solo.data(), li.solo.size() * sizeof(SoloTask));
-            if (rc == DTANS_OK) {
-                // partial slots of solo tasks are written for one lane only
-                cudaError_t me = cudaMemset(h->base.partials, 0, pa_b);
-                if (me != cudaSuccess) rc = cuda_fail(me, "memset partials");
-            }
+            // partial slots of solo tasks are written for one lane only
+            zero(h->base.partials, pa_b);
             cp(lb + tb_b, li.pool.data(), li.pool.size() * 4);
             cp(lb + tb_b + pl_b, li.slices.data(), li.slices.size() * sizeof(LongSlice));
         }
     }
-    if (rc == DTANS_OK && nsl > 0) {
-        // skewed slice costs -> dynamic longest-first scheduling
-        std::vector<uint32_t> cost((size_t)nsl);
-        double mean = 0;
-        uint32_t mx = 0;
-        for (int64_t s = 0; s < nsl; s++) {
-            uint32_t m = 0;
-            for (int64_t i = s * kSlice; i < std::min<int64_t>((s + 1) * kSlice, c->rows); i++)
-                m = std::max(m, c->row_symbols[i]);
-            cost[s] = (m + 7) / 8;
-            const uint64_t words = ((c->directory[s + 1] + 3) & ~3ull) - (c->directory[s] & ~3ull);
-            if (cost[s] > h->base.long_seg || words > h->long_words) cost[s] = 0;  // task-decoded
-            mean += cost[s];
-            mx = std::max(mx, cost[s]);
-        }
-        mean /= (double)nsl;
-        const char *ed = getenv("DTANS_DYNAMIC");
-        const bool dyn = ed ? atoi(ed) != 0 : (mx > 4.0 * std::max(mean, 1.0));
-        h->base.dynamic = dyn ? 1 : 0;
-        bool sorted = true;
-        for (int64_t s = 1; s < nsl && sorted; s++) sorted = cost[s] <= cost[s - 1];
-        if (dyn && !sorted) {
-            std::vector<uint32_t> order((size_t)nsl);
-            for (int64_t s = 0; s < nsl; s++) order[s] = (uint32_t)s;
-            std::stable_sort(order.begin(), order.end(), [&](uint32_t p, uint32_t q) { return cost[p] > cost[q]; });
-            cudaError_t ce = cudaMalloc(&h->d_order, sizeof(uint32_t) * order.size());
-            if (ce != cudaSuccess) rc = cuda_fail(ce, "cudaMalloc slice order");
-            else {
-                cp(h->d_order, order.data(), sizeof(uint32_t) * order.size());
-                h->base.slice_order = h->d_order;
-            }
-        }
-    }
     if (rc == DTANS_OK)
-        rc = c->precision == 8 ? configure<double>(h, tb, c->directory) : configure<float>(h, tb, c->directory);
+        rc = c->precision == 8 ? configure<double>(h, tb, sp) : configure<float>(h, tb, sp);
     if (rc != DTANS_OK) {
         cudaFree(h->d_base);
         if (h->d_long) cudaFree(h->d_long);
-        if (h->d_order) cudaFree(h->d_order);
         delete h;
         return rc;
     }
@@ -468,7 +636,6 @@ extern "C" void dtans_free(dtans_dev *h)
     if (h->d_base) cudaFree(h->d_base);
     if (h->d_long) cudaFree(h->d_long);
     if (h->d_row_map) cudaFree(h->d_row_map);
-    if (h->d_order) cudaFree(h->d_order);
     if (h->d_io) cudaFree(h->d_io);
     for (int k = 0; k < kHostChunks; k++) {
         if (h->ev_in[k]) cudaEventDestroy(h->ev_in[k]);
@@ -542,6 +709,7 @@ extern "C" int dtans_check(dtans_dev *h, void *stream)
     CK(cudaMemcpy(&err, h->d_err, sizeof(err), cudaMemcpyDeviceToHost), "read error word");
     if (err) {
         CK(cudaMemset(h->d_err, 0, sizeof(err)), "clear error word");
+        if (err & 4u) return fail(DTANS_E_CUDA, "shared-memory window not 16 KB aligned at the slot tables");
         if (err & 1u) return fail(DTANS_E_CORRUPT, "slice consumed an unexpected number of words");
         return fail(DTANS_E_CORRUPT, "decoded column index out of range");
     }
@@ -568,7 +736,8 @@ extern "C" int dtans_spmv_host(dtans_dev *h, const void *x, const void *y, void 
     // kernel on that range (compute stream) and y' out (copy-out stream), so
     // the D2H of a chunk overlaps the H2D and decode of the next.  Containers
     // with long slices or dynamic scheduling use one launch.
-    const bool chunked = h->base.nlong == 0 && !h->base.dynamic && h->nslices >= 64 * kHostChunks;
+    const int64_t nchunks = (int64_t)h->chunks.size();
+    const bool chunked = h->base.nlong == 0 && !h->base.dynamic && nchunks >= 64 * kHostChunks;
     if (!h->st_in) {
         CK(cudaStreamCreateWithFlags(&h->st_in, cudaStreamNonBlocking), "stream");
         CK(cudaStreamCreateWithFlags(&h->st_comp, cudaStreamNonBlocking), "stream");
@@ -581,15 +750,21 @@ extern "C" int dtans_spmv_host(dtans_dev *h, const void *x, const void *y, void 
     const int nch = chunked ? kHostChunks : 1;
     CK(cudaMemcpyAsync(dx, x, es * (size_t)h->cols, cudaMemcpyHostToDevice, h->st_in), "H2D x");
     for (int k = 0; k < nch; k++) {
-        const int64_t s0 = h->nslices * k / nch, s1 = h->nslices * (k + 1) / nch;
-        const int64_t r0 = s0 * kSlice, r1 = std::min<int64_t>(s1 * kSlice, h->rows);
+        // chunks [c0, c1) cover rows [r0, r1) (natural order when chunked)
+        const int64_t c0 = nchunks * k / nch, c1 = nchunks * (k + 1) / nch;
+        int64_t r0 = 0, r1 = h->rows;
+        if (chunked) {
+            r0 = (int64_t)h->chunks[c0].s0 * kSlice;
+            const dev::ChunkRec &last = h->chunks[c1 - 1];
+            r1 = std::min<int64_t>(((int64_t)last.s0 + (last.kw & 0xFF)) * kSlice, h->rows);
+        }
         if (y && r1 > r0)
             CK(cudaMemcpyAsync(dy + es * r0, (const char *)y + es * r0, es * (size_t)(r1 - r0),
                                cudaMemcpyHostToDevice, h->st_in), "H2D y");
         CK(cudaEventRecord(h->ev_in[k], h->st_in), "event");
         CK(cudaStreamWaitEvent(h->st_comp, h->ev_in[k], 0), "wait");
         int rc;
-        const int64_t lo = chunked ? s0 : -1, hi = chunked ? s1 : -1;
+        const int64_t lo = chunked ? c0 : -1, hi = chunked ? c1 : -1;
         if (h->precision == 8)
             rc = launch<double>(h, (const double *)dx, y ? (const double *)dy : nullptr, (double *)dout,
                                 nullptr, nullptr, nullptr, false, h->st_comp, lo, hi);
@@ -599,9 +774,8 @@ extern "C" int dtans_spmv_host(dtans_dev *h, const void *x, const void *y, void 
         if (rc) return rc;
         CK(cudaEventRecord(h->ev_done[k], h->st_comp), "event");
         CK(cudaStreamWaitEvent(h->st_out, h->ev_done[k], 0), "wait");
-        const int64_t q0 = chunked ? r0 : 0, q1 = chunked ? r1 : h->rows;
-        if (q1 > q0)
-            CK(cudaMemcpyAsync((char *)out + es * q0, dout + es * q0, es * (size_t)(q1 - q0),
+        if (r1 > r0)
+            CK(cudaMemcpyAsync((char *)out + es * r0, dout + es * r0, es * (size_t)(r1 - r0),
                                cudaMemcpyDeviceToHost, h->st_out), "D2H out");
     }
     CK(cudaStreamSynchronize(h->st_out), "synchronize");

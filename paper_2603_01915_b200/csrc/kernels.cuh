@@ -12,14 +12,23 @@
 // from +0.0 (container.py:534-551) with __dmul_rn/__dadd_rn, so the result
 // is bitwise the reference's.
 //
-// Memory.  Each warp owns a ring of kRing shared-memory buffers; lane 0
-// stages the word range [directory[s], directory[s+1]) of the slice it will
-// decode kRing slices later with one cp.async.bulk (TMA bulk copy, 16-byte
-// aligned window) completing on an mbarrier.  The decoder then reads stream
-// words from shared memory.  Slices larger than a buffer are read straight
-// from global memory (same code, generic pointer).  Slot tables are compact
-// u32 entries {digit:8, base-1:8, id:16} per domain (16 KB each) plus
-// dictionaries of the retained symbols, so a CTA needs ~33 KB of tables.
+// Work unit: a chunk = a run of consecutive slices (host-built list, sized
+// to a staging buffer).  Each warp owns a ring of shared-memory buffers;
+// lane 0 stages a chunk with three cp.async.bulk copies (TMA bulk engine)
+// completing on one mbarrier: the chunk's directory entries, its
+// row_symbols, and the 16-byte aligned stream window [dir[s0], dir[s0+k]).
+// The decoder then reads everything except x, y and the output from shared
+// memory.  Slices that do not fit a buffer (or whose rows are very long) are
+// "long" slices, decoded by the checkpointed task kernels instead.
+//
+// Shared-memory tables.  The two 4096-entry slot tables sit at fixed
+// offsets 0 and 16384 (compile-time immediates in LDS), entries
+// {digit:8, base-1:8, F:16}.  F is the byte offset of the slot's symbol in
+// its dictionary, or, for the delta domain when every retained delta is
+// < 0xFFFF, the delta itself ("inline" deltas: no dictionary access).  The
+// dictionaries are replicated R times, element e of copy c at (e*R + c)*w
+// bytes, and lane i reads copy i % R: with R = 16 (f64) / 32 (f32) a warp's
+// 32 random dictionary reads are bank-conflict free.
 //
 // Mixed-radix state.  At every segment start d < r < 2^32 (r is divided by
 // 2^32 whenever it reaches 2^32), so the resting state is two u32.  A group
@@ -38,8 +47,16 @@ namespace dev {
 
 constexpr int kSliceRows = 32;
 constexpr int kSlots = 4096;
-constexpr int kMaxWarps = 32;  // per CTA (1024 threads); smem layout is sized for this
-constexpr int kRing = 3;
+#ifndef DTANS_CTA_WARPS
+#define DTANS_CTA_WARPS 32
+#endif
+constexpr int kMaxWarps = DTANS_CTA_WARPS;  // warps per CTA of the main kernel
+constexpr int kMaxRing = 3;     // staging buffers per warp (runtime 2 or 3)
+constexpr int kMaxChunk = 16;   // slices per chunk
+constexpr uint32_t kTabBytes = 2 * kSlots * 4;
+constexpr uint32_t kDeltaInlineEsc = 0xFFFF0000u;  // inline deltas: F = 0xFFFF marks an escape
+
+extern __shared__ __align__(1024) unsigned char dtans_smem[];
 
 template <typename V> struct ValueTraits;
 template <> struct ValueTraits<double> {
@@ -57,17 +74,33 @@ template <> struct ValueTraits<float> {
     __device__ static inline float add(float a, float b) { return __fadd_rn(a, b); }
 };
 
+// A chunk: slices [s0, s0 + k) (k = kw & 0xFF) stored as one contiguous
+// blob of kw >> 8 words at word offset `off` of the chunk-blob array:
+//   [hdr: k+1 u32 stream offsets, padded to 4][row_symbols: k*32 u32][stream words, padded to 4]
+// hdr[i] = directory[s0+i] - directory[s0] (the reference's word ranges,
+// container.py:296-317, relative to the chunk).
+struct __align__(16) ChunkRec {
+    unsigned long long off;
+    uint32_t s0;
+    uint32_t kw;
+};
+__host__ __device__ constexpr uint32_t chunk_hdr_words(uint32_t k) { return (k + 4u) & ~3u; }
+
 struct KernelArgs {
-    const uint32_t *tables;       // [dtab 4096][vtab 4096][ddict][vdict] (global copy)
+    const uint32_t *tables;       // shared-memory image [off_img, off_img + table_bytes) (global copy)
     int32_t table_bytes;          // bytes to copy into shared memory (multiple of 16)
-    int32_t off_ddict, off_vdict; // byte offsets inside the table block
-    uint32_t desc_min, vesc_min;  // entry >= this  <=>  escape (id == n_retained)
+    int32_t off_img, off_tab;     // image start; delta slot table (16 KB aligned address), value table +16 KB
+    int32_t off_ddict, off_vdict; // byte offsets in shared memory (replicated dictionaries)
+    int32_t rep_d, rep_v;         // replication factors (powers of two)
+    uint32_t desc_min, vesc_min;  // entry >= this  <=>  escape
     int32_t pads_ok;              // both domains retain a pad symbol
-    int32_t off_bars, off_meta, off_bufs;  // shared-memory layout
-    int32_t bufw;                 // words per stream buffer
-    const uint32_t *row_symbols;  // rows
-    const uint64_t *directory;    // nslices + 1
-    const uint32_t *stream;       // nwords (+ 64 B padding)
+    int32_t off_bars, off_meta, off_ctl, off_bufs;  // shared-memory layout
+    int32_t bufb;                 // bytes per staging buffer (multiple of 16)
+    int32_t nring;                // staging buffers per warp (2 or 3)
+    const uint32_t *blob;         // chunk blobs (main kernel)
+    const uint32_t *row_symbols;  // rows (long-slice kernels only)
+    const uint64_t *directory;    // nslices + 1 (long-slice kernels only)
+    const uint32_t *stream;       // nwords + kStreamPadWords (long-slice kernels only)
     int64_t rows, cols, nslices, nwords;
     const void *x;
     const void *y;                // may be null (y' = A x)
@@ -77,8 +110,6 @@ struct KernelArgs {
     void *dec_vals;               // decode kernel only
     unsigned int *err;            // bit 0: consumption mismatch, bit 1: column OOB
     // long slices (checkpoint index, checkpoints.cpp)
-    uint32_t long_seg;            // slices with more segments go to the task kernel
-    uint32_t long_words;          // ... and slices with more stream words
     uint32_t ntasks, nlong, nsolo;
     uint32_t nlong_small, nlong_small_blocks;  // finalize: slices with <= 32 partials come first
     int32_t single_direct;                      // single-task slices write y' in the task kernel
@@ -88,11 +119,11 @@ struct KernelArgs {
     const LongSlice *longs;
     void *partials;               // V[nparts][32]
     const uint32_t *row_map;      // optional: y/out index of encoded row i (row-reordered P*A)
-    // work distribution
+    // work distribution over the chunk list
+    const ChunkRec *chunks;
+    uint32_t chunk_lo, chunk_hi;  // chunks of this launch
     int32_t dynamic;              // 1: atomic ticket counter instead of a static stride
-    uint32_t slice_lo, slice_hi;  // static order: slices [slice_lo, slice_hi) of this launch
     uint32_t *work_counter;       // zeroed before every dynamic launch
-    const uint32_t *slice_order;  // optional: ticket -> slice (longest first)
 };
 
 __device__ __forceinline__ uint32_t lanemask_lt()
@@ -107,24 +138,60 @@ __device__ __forceinline__ uint32_t smem_u32(const void *p)
     return (uint32_t)__cvta_generic_to_shared(p);
 }
 
-__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count)
+// Shared-memory loads at absolute 32-bit shared addresses (ld.shared with
+// a register + immediate address).
+__device__ __forceinline__ uint32_t sh32(uint32_t addr)
 {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
+    return v;
+}
+__device__ __forceinline__ unsigned long long sh64(uint32_t addr)
+{
+    unsigned long long v;
+    asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(addr) : "memory");
+    return v;
+}
+// Tables and dictionaries never change after the CTA prologue: plain
+// (non-volatile) loads the compiler may schedule freely.
+__device__ __forceinline__ uint32_t tab32(uint32_t addr)
+{
+    uint32_t v;
+    asm("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+    return v;
+}
+__device__ __forceinline__ uint32_t vtab32(uint32_t addr)
+{
+    uint32_t v;
+    asm("ld.shared.u32 %0, [%1+16384];" : "=r"(v) : "r"(addr));
+    return v;
+}
+template <typename Bits> __device__ __forceinline__ Bits dict_bits(uint32_t addr);
+template <> __device__ __forceinline__ unsigned long long dict_bits<unsigned long long>(uint32_t addr)
+{
+    unsigned long long v;
+    asm("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(addr));
+    return v;
+}
+template <> __device__ __forceinline__ uint32_t dict_bits<uint32_t>(uint32_t addr) { return tab32(addr); }
+
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
 }
 
-__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t bytes)
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint32_t bar, uint32_t bytes)
 {
-    asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-                 "r"(bytes)
+    asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
                  : "memory");
 }
 
-__device__ __forceinline__ void mbar_arrive(uint64_t *bar)
+__device__ __forceinline__ void mbar_arrive(uint32_t bar)
 {
-    asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+    asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
 
-__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity)
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity)
 {
     asm volatile(
         "{\n"
@@ -132,23 +199,17 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity)
         "WAIT_%=:\n"
         "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%0], %1;\n"
         "@!p bra WAIT_%=;\n"
-        "}\n" ::"r"(smem_u32(bar)),
+        "}\n" ::"r"(bar),
         "r"(parity)
         : "memory");
 }
 
-__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar)
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void *src, uint32_t bytes, uint32_t bar)
 {
     asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-            smem_u32(dst)),
-        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+        "l"(src), "r"(bytes), "r"(bar)
         : "memory");
-}
-
-__device__ __forceinline__ void fence_proxy_async()
-{
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
 __device__ __forceinline__ void fence_mbar_init()
@@ -156,134 +217,97 @@ __device__ __forceinline__ void fence_mbar_init()
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }
 
-__device__ __forceinline__ uint32_t lds32(uint32_t addr)
-{
-    uint32_t v;
-    asm("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
-    return v;
-}
-
-__device__ __forceinline__ unsigned long long lds64(uint32_t addr)
-{
-    unsigned long long v;
-    asm("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(addr));
-    return v;
-}
-
-// Stream words that change between slices (TMA-written): volatile so they
-// are never hoisted across the mbarrier wait.
-__device__ __forceinline__ uint32_t lds32_v(uint32_t addr)
-{
-    uint32_t v;
-    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
-    return v;
-}
-
-template <typename Bits> __device__ __forceinline__ Bits lds_bits(uint32_t addr);
-template <> __device__ __forceinline__ unsigned long long lds_bits<unsigned long long>(uint32_t addr)
-{
-    return lds64(addr);
-}
-template <> __device__ __forceinline__ uint32_t lds_bits<uint32_t>(uint32_t addr) { return lds32(addr); }
-
 // Word sources for one slice, addressed by the position relative to
 // directory[s] (32-bit): the staged shared-memory window or global memory.
 // Reads are not clamped: a segment consumes at most kSegMaxWords words, the
 // decoder stops as soon as its cursor passes the slice end (then reports
-// CorruptStream), and both the shared ring and the device stream carry at
-// least kOverrunWords of slack, so a corrupt container can never read
+// CorruptStream), and both the staging buffers and the device stream carry
+// at least kOverrunWords of slack, so a corrupt container can never read
 // outside the allocations.
 constexpr uint32_t kSegMaxWords = 32u * 15u;  // payload 12 + 2 checks + 1 uncond per lane
 constexpr uint32_t kOverrunWords = 3u * 32u + kSegMaxWords + 64u;
 constexpr uint32_t kStreamPadWords = kOverrunWords;  // device stream padding
 struct SmemSrc {
     uint32_t addr;  // shared address of word directory[s]
-    __device__ __forceinline__ uint32_t operator()(uint32_t rel) const { return lds32_v(addr + rel * 4u); }
-    __device__ __forceinline__ void advance(uint32_t, int) {}
+    __device__ __forceinline__ uint32_t operator()(uint32_t rel) const { return sh32(addr + rel * 4u); }
 };
 struct GmemSrc {
     const uint32_t *p;  // &stream[directory[s]]
     __device__ __forceinline__ uint32_t operator()(uint32_t rel) const { return __ldg(p + rel); }
-    __device__ __forceinline__ void advance(uint32_t, int) {}
 };
 
-
-// Per-buffer slice record written by the stager: the slice's word offset
-// inside the 16-byte aligned staged window (bit 31: not staged, read from
-// global memory instead) and its word count.
-struct SliceMeta {
-    uint32_t off;     // words from the window start to directory[s]; bit 31 = global
-    uint32_t nwords;  // directory[s+1] - directory[s]
-    uint32_t slice;   // slice id (kNoSlice: the warp's work is exhausted)
-    uint32_t pad;
-};
-constexpr uint32_t kNoSlice = 0xFFFFFFFFu;
-constexpr uint32_t kGlobalSlice = 0x80000000u;
-
-// Stage a slice (directory entries lo, hi prefetched) into a ring buffer
-// (lane 0 only).  The previous contents were consumed by this warp's LDS
-// before the __syncwarp that precedes the call (the same WAR ordering a
-// CUTLASS TMA pipeline relies on), so no proxy fence is issued.
-__device__ __forceinline__ void stage_slice(const KernelArgs &a, uint32_t s, uint64_t lo, uint64_t hi,
-                                            uint64_t *bar, SliceMeta *meta, uint32_t *buf)
-{
-    if (s == kNoSlice) {
-        *meta = SliceMeta{0u, 0u, kNoSlice, 0u};
-        mbar_arrive(bar);
-        return;
-    }
-    const uint64_t abase = lo & ~3ull;
-    const uint32_t words = (uint32_t)(((hi + 3) & ~3ull) - abase);
-    const bool staged = words > 0 && words <= (uint32_t)a.bufw;
-    *meta = SliceMeta{(uint32_t)(lo - abase) | (staged ? 0u : kGlobalSlice), (uint32_t)(hi - lo), s, 0u};
-    if (staged) {
-        mbar_arrive_expect_tx(bar, words * 4u);
-        bulk_g2s(buf, a.stream + abase, words * 4u, bar);
-    } else {
-        mbar_arrive(bar);
-    }
-}
-
+// Per-lane shared-memory context (absolute shared addresses).  The delta
+// slot table starts on a 16 KB boundary, so a slot's address is one LOP3:
+// (bits & 0x3FFC) | tab; the value table follows at +16384.
 struct Ctx {
-    uint32_t dtab, vtab, ddict, vdict;  // shared addresses
+    uint32_t tab;                       // shared address of the delta slot table
+    uint32_t dbase, vbase;              // dictionary + this lane's copy
     uint32_t desc_min, vesc_min;        // entry >= this <=> escape
     uint32_t cols_m1;
     uint32_t lt;                        // lanemask_lt
     bool pads_ok;
 };
 
-__device__ __forceinline__ void slot_offsets(uint32_t w0, uint32_t w1, uint32_t w2, uint32_t so[8])
+template <typename V>
+__device__ __forceinline__ Ctx make_ctx(const KernelArgs &a, int lane)
 {
-    // unpack (codec.py:148-162): slot k = bits [12k, 12k+12) of w0:w1:w2, as
-    // byte offsets (slot * 4) into the u32 slot tables
-    so[0] = (w2 << 2) & 0x3FFCu;
-    so[1] = (w2 >> 10) & 0x3FFCu;
-    so[2] = __funnelshift_r(w2, w1, 22) & 0x3FFCu;
-    so[3] = (w1 >> 2) & 0x3FFCu;
-    so[4] = (w1 >> 14) & 0x3FFCu;
-    so[5] = __funnelshift_r(w1, w0, 26) & 0x3FFCu;
-    so[6] = (w0 >> 6) & 0x3FFCu;
-    so[7] = (w0 >> 18) & 0x3FFCu;
+    const uint32_t sb = smem_u32(dtans_smem);
+    Ctx C;
+    C.tab = sb + (uint32_t)a.off_tab;
+    C.dbase = sb + (uint32_t)a.off_ddict + (uint32_t)(lane & (a.rep_d - 1)) * 4u;
+    C.vbase = sb + (uint32_t)a.off_vdict + (uint32_t)(lane & (a.rep_v - 1)) * (uint32_t)sizeof(V);
+    C.desc_min = a.desc_min;
+    C.vesc_min = a.vesc_min;
+    C.cols_m1 = (uint32_t)(a.cols - 1);
+    C.lt = lanemask_lt();
+    C.pads_ok = a.pads_ok != 0;
+    return C;
 }
 
-// Table entries of pair p and the dictionary symbols they point at (escape
-// entries point at a dummy dictionary slot; the payload overwrites them).
-template <typename Bits>
+// Copy the table image into shared memory (all threads; caller syncs).
+// Returns false if the tables are not 16 KB aligned in the shared window
+// (the kernel then reports an error instead of decoding).
+__device__ __forceinline__ bool load_tables(const KernelArgs &a)
+{
+    const int4 *src = reinterpret_cast<const int4 *>(a.tables);
+    int4 *dst = reinterpret_cast<int4 *>(dtans_smem + a.off_img);
+    for (int i = threadIdx.x; i < a.table_bytes / 16; i += blockDim.x) dst[i] = __ldg(src + i);
+    return ((smem_u32(dtans_smem) + (uint32_t)a.off_tab) & 0x3FFFu) == 0u;
+}
+
+__device__ __forceinline__ void slot_offsets(const uint32_t tab, uint32_t w0, uint32_t w1, uint32_t w2,
+                                             uint32_t so[8])
+{
+    // unpack (codec.py:148-162): slot k = bits [12k, 12k+12) of w0:w1:w2, as
+    // shared addresses tab + slot * 4 (tab is 16 KB aligned: OR == ADD)
+    so[0] = ((w2 << 2) & 0x3FFCu) | tab;
+    so[1] = ((w2 >> 10) & 0x3FFCu) | tab;
+    so[2] = (__funnelshift_r(w2, w1, 22) & 0x3FFCu) | tab;
+    so[3] = ((w1 >> 2) & 0x3FFCu) | tab;
+    so[4] = ((w1 >> 14) & 0x3FFCu) | tab;
+    so[5] = (__funnelshift_r(w1, w0, 26) & 0x3FFCu) | tab;
+    so[6] = ((w0 >> 6) & 0x3FFCu) | tab;
+    so[7] = ((w0 >> 18) & 0x3FFCu) | tab;
+}
+
+// Table entries of pair p and the symbols they decode to (escape entries
+// point at a dummy dictionary slot / carry 0xFFFF; the payload overwrites
+// them).
+template <typename Bits, bool kDIn>
 __device__ __forceinline__ void lookup_pair(const Ctx &C, uint32_t sod, uint32_t sov, uint32_t &ed, uint32_t &ev,
                                             uint32_t &ds, Bits &vs)
 {
-    ed = lds32(C.dtab + sod);
-    ev = lds32(C.vtab + sov);
-    ds = lds32(C.ddict + (ed >> 16));  // id field = byte offset into the dictionary
-    vs = lds_bits<Bits>(C.vdict + (ev >> 16));
+    ed = tab32(sod);
+    ev = vtab32(sov);
+    ds = kDIn ? (ed >> 16) : tab32(C.dbase + (ed >> 16));
+    vs = dict_bits<Bits>(C.vbase + (ev >> 16));
 }
 
 // Payload event (container.py:459-470): per-lane word counts, exclusive warp
 // scan, words read in slot order, low word first, overwriting the symbols.
 template <typename T, class Src>
 __device__ __forceinline__ void payload_event(const Ctx &C, const Src &src, uint32_t &cur, const bool act,
-                                              const uint32_t e[8], uint32_t ds[4], typename T::Bits vs[4],
-                                              const int lane)
+                                              const uint32_t e[8], uint32_t ds[4], typename T::Bits vs[4])
 {
     using Bits = typename T::Bits;
     // cheap test first: escape entries are the largest entries of a table
@@ -317,10 +341,9 @@ __device__ __forceinline__ void payload_event(const Ctx &C, const Src &src, uint
     const uint32_t b0 = __ballot_sync(0xFFFFFFFFu, pc & 1u);
     const uint32_t excl = __popc(b0 & C.lt) + (__popc(b1 & C.lt) << 1) + (__popc(b2 & C.lt) << 2) +
                           (__popc(b3 & C.lt) << 3);
-    const uint32_t incl = excl + pc;
     const uint32_t total = __popc(b0) + (__popc(b1) << 1) + (__popc(b2) << 2) + (__popc(b3) << 3);
     if (pc) {
-        uint32_t off = cur + (incl - pc);
+        uint32_t off = cur + excl;
 #pragma unroll
         for (int p = 0; p < 4; p++) {
             if (e[2 * p] >= C.desc_min) {
@@ -372,20 +395,20 @@ __device__ __forceinline__ void mad_wide(uint32_t a, uint32_t b, uint32_t c_lo, 
         : "r"(c_lo), "r"(c_hi), "r"(a), "r"(b));
 }
 
-// d*B + D with B-1 = bm1 (< 2^32), d < 2^32, D < 2^32: d*bm1 + (d + D).
+// d*B + D with B-1 = bm1 (< 2^32), d < 2^32, D < 2^32: (d*bm1 + D) + d.
 __device__ __forceinline__ void fold(uint32_t d, uint32_t bm1, uint32_t D, uint32_t &lo, uint32_t &hi)
 {
-    uint32_t s_lo, s_hi;
-    asm("add.cc.u32 %0, %2, %3;\naddc.u32 %1, 0, 0;" : "=r"(s_lo), "=r"(s_hi) : "r"(d), "r"(D));
-    mad_wide(d, bm1, s_lo, s_hi, lo, hi);
+    uint32_t t_lo, t_hi;
+    mad_wide(d, bm1, D, 0u, t_lo, t_hi);
+    asm("add.cc.u32 %0, %2, %3;\naddc.u32 %1, %4, 0;" : "=r"(lo), "=r"(hi) : "r"(t_lo), "r"(d), "r"(t_hi));
 }
 
 // One segment that is not the final one of the slice (some lane folds
 // digits).  kHot: every lane is active and not in its last segment (all
 // 4 pairs valid, all lanes load/extract), so the per-lane predicates vanish.
-template <typename V, bool kDecode, bool kHot, class Src>
+template <typename V, bool kDecode, bool kHot, bool kDIn, class Src>
 __device__ __forceinline__ void full_segment(const KernelArgs &a, const Ctx &C, const V *__restrict__ x,
-                                             Src &src, const uint32_t j, const uint32_t n,
+                                             const Src &src, const uint32_t j, const uint32_t n,
                                              const uint32_t nseg, uint32_t &w0, uint32_t &w1, uint32_t &w2,
                                              uint32_t &d, uint32_t &r, uint32_t &cur, uint32_t &col, V &acc,
                                              int64_t &out_pos, const int lane)
@@ -397,15 +420,17 @@ __device__ __forceinline__ void full_segment(const KernelArgs &a, const Ctx &C, 
     const bool notlast = kHot || j + 1 < nseg;
     uint32_t so[8], e[8], ds[4];
     Bits vs[4];
-    slot_offsets(w0, w1, w2, so);
+    slot_offsets(C.tab, w0, w1, w2, so);
 #pragma unroll
-    for (int p = 0; p < 4; p++) lookup_pair<Bits>(C, so[2 * p], so[2 * p + 1], e[2 * p], e[2 * p + 1], ds[p], vs[p]);
-    payload_event<T>(C, src, cur, act, e, ds, vs, lane);
+    for (int p = 0; p < 4; p++)
+        lookup_pair<Bits, kDIn>(C, so[2 * p], so[2 * p + 1], e[2 * p], e[2 * p + 1], ds[p], vs[p]);
+    payload_event<T>(C, src, cur, act, e, ds, vs);
     V xv[4];
 #pragma unroll
     for (int p = 0; p < 4; p++) {
         const bool valid = kHot || 8u * j + 2u * p < n;
-        if (kHot) {
+        xv[p] = V(0);
+        if (valid) {
             col += ds[p];
             if (kDecode) {
                 a.dec_cols[out_pos] = (int64_t)col;
@@ -413,18 +438,6 @@ __device__ __forceinline__ void full_segment(const KernelArgs &a, const Ctx &C, 
                 out_pos++;
             } else {
                 xv[p] = __ldg(x + min(col, C.cols_m1));
-            }
-        } else {
-            xv[p] = V(0);
-            if (valid) {
-                col += ds[p];
-                if (kDecode) {
-                    a.dec_cols[out_pos] = (int64_t)col;
-                    reinterpret_cast<Bits *>(a.dec_vals)[out_pos] = vs[p];
-                    out_pos++;
-                } else {
-                    xv[p] = __ldg(x + min(col, C.cols_m1));
-                }
             }
         }
     }
@@ -461,11 +474,7 @@ __device__ __forceinline__ void full_segment(const KernelArgs &a, const Ctx &C, 
     if (!kDecode) {
 #pragma unroll
         for (int p = 0; p < 4; p++) {
-            if (kHot) {
-                acc = T::add(acc, T::mul(T::from_bits(vs[p]), xv[p]));
-            } else if (8u * j + 2u * p < n) {
-                acc = T::add(acc, T::mul(T::from_bits(vs[p]), xv[p]));
-            }
+            if (kHot || 8u * j + 2u * p < n) acc = T::add(acc, T::mul(T::from_bits(vs[p]), xv[p]));
         }
     }
 }
@@ -483,28 +492,28 @@ template <typename V> struct LaneState {
 // with any valid position in the warp (compile-time, so no per-pair
 // branches); slots past them are pads that only matter if they can escape,
 // in which case the caller passes NP = 4.
-template <typename V, bool kDecode, int NP, class Src>
-__device__ __forceinline__ void final_segment(const KernelArgs &a, const Ctx &C, const V *__restrict__ x, Src &src,
-                                              const uint32_t jf, const uint32_t n, const uint32_t maxn,
-                                              LaneState<V> &st, const int lane)
+template <typename V, bool kDecode, bool kDIn, int NP, class Src>
+__device__ __forceinline__ void final_segment(const KernelArgs &a, const Ctx &C, const V *__restrict__ x,
+                                              const Src &src, const uint32_t jf, const uint32_t n,
+                                              LaneState<V> &st)
 {
     using T = ValueTraits<V>;
     using Bits = typename T::Bits;
     const bool act = jf < ((n + 7u) >> 3);
     uint32_t so[8], e[8], ds[4];
     Bits vs[4];
-    slot_offsets(st.w0, st.w1, st.w2, so);
+    slot_offsets(C.tab, st.w0, st.w1, st.w2, so);
 #pragma unroll
     for (int p = 0; p < 4; p++) {
         if (p < NP) {
-            lookup_pair<Bits>(C, so[2 * p], so[2 * p + 1], e[2 * p], e[2 * p + 1], ds[p], vs[p]);
+            lookup_pair<Bits, kDIn>(C, so[2 * p], so[2 * p + 1], e[2 * p], e[2 * p + 1], ds[p], vs[p]);
         } else {
             e[2 * p] = e[2 * p + 1] = 0u;
             ds[p] = 0u;
             vs[p] = 0;
         }
     }
-    payload_event<T>(C, src, st.cur, act, e, ds, vs, lane);
+    payload_event<T>(C, src, st.cur, act, e, ds, vs);
     const uint32_t base = 8u * jf;
 #pragma unroll
     for (int p = 0; p < NP; p++) {
@@ -520,7 +529,6 @@ __device__ __forceinline__ void final_segment(const KernelArgs &a, const Ctx &C,
             }
         }
     }
-    (void)maxn;
 }
 
 // Segments [j0, j1) of a slice (j1 <= max_nseg).  If j1 == max_nseg the
@@ -528,14 +536,12 @@ __device__ __forceinline__ void final_segment(const KernelArgs &a, const Ctx &C,
 // so no digits are folded and no checks/unconditional loads happen, and
 // pairs past the longest row are skipped (pads need lookups only when they
 // may escape).  Returns false if the cursor ran past `end` (corrupt slice).
-template <typename V, bool kDecode, class Src>
+template <typename V, bool kDecode, bool kDIn, class Src>
 __device__ __forceinline__ bool decode_range(const KernelArgs &a, const Ctx &C, const V *__restrict__ x,
-                                             Src &src, const uint32_t end, const uint32_t n,
+                                             const Src &src, const uint32_t end, const uint32_t n,
                                              const uint32_t maxn, const uint32_t j0, const uint32_t j1,
                                              LaneState<V> &st, const int lane)
 {
-    using T = ValueTraits<V>;
-    using Bits = typename T::Bits;
     const uint32_t FULL = 0xFFFFFFFFu;
     const uint32_t nseg = (n + 7u) >> 3;
     const uint32_t max_nseg = (maxn + 7u) >> 3;
@@ -546,28 +552,25 @@ __device__ __forceinline__ bool decode_range(const KernelArgs &a, const Ctx &C, 
     uint32_t j = j0;
     const uint32_t jhot = min(jfull, min_nseg > 0 ? min_nseg - 1u : 0u);
     for (; j < jhot; j++) {
-        src.advance(st.cur, lane);
-        full_segment<V, kDecode, true>(a, C, x, src, j, n, nseg, st.w0, st.w1, st.w2, st.d, st.r, st.cur, st.col,
-                                       st.acc, st.out_pos, lane);
+        full_segment<V, kDecode, true, kDIn>(a, C, x, src, j, n, nseg, st.w0, st.w1, st.w2, st.d, st.r, st.cur,
+                                             st.col, st.acc, st.out_pos, lane);
         if (st.cur > end) return false;  // uniform
     }
     for (; j < jfull; j++) {
-        src.advance(st.cur, lane);
-        full_segment<V, kDecode, false>(a, C, x, src, j, n, nseg, st.w0, st.w1, st.w2, st.d, st.r, st.cur,
-                                        st.col, st.acc, st.out_pos, lane);
+        full_segment<V, kDecode, false, kDIn>(a, C, x, src, j, n, nseg, st.w0, st.w1, st.w2, st.d, st.r,
+                                              st.cur, st.col, st.acc, st.out_pos, lane);
         if (st.cur > end) return false;
     }
     if (j1 == max_nseg && max_nseg > 0) {
-        src.advance(st.cur, lane);
         // pairs the final segment needs: (maxn - 8 jf) / 2 (n is even); all 4
         // lookups are needed only when pads may escape (escape-only table)
         const uint32_t jf = max_nseg - 1;
         const uint32_t np = C.pads_ok ? (maxn - 8u * jf) >> 1 : 4u;
         switch (np) {  // uniform
-        case 1: final_segment<V, kDecode, 1>(a, C, x, src, jf, n, maxn, st, lane); break;
-        case 2: final_segment<V, kDecode, 2>(a, C, x, src, jf, n, maxn, st, lane); break;
-        case 3: final_segment<V, kDecode, 3>(a, C, x, src, jf, n, maxn, st, lane); break;
-        default: final_segment<V, kDecode, 4>(a, C, x, src, jf, n, maxn, st, lane); break;
+        case 1: final_segment<V, kDecode, kDIn, 1>(a, C, x, src, jf, n, st); break;
+        case 2: final_segment<V, kDecode, kDIn, 2>(a, C, x, src, jf, n, st); break;
+        case 3: final_segment<V, kDecode, kDIn, 3>(a, C, x, src, jf, n, st); break;
+        default: final_segment<V, kDecode, kDIn, 4>(a, C, x, src, jf, n, st); break;
         }
     }
     return true;
@@ -575,7 +578,7 @@ __device__ __forceinline__ bool decode_range(const KernelArgs &a, const Ctx &C, 
 
 // init events (container.py:426-429): 3 words per active lane
 template <typename V, class Src>
-__device__ __forceinline__ void init_state(const Ctx &C, Src &src, const uint32_t n, LaneState<V> &st)
+__device__ __forceinline__ void init_state(const Ctx &C, const Src &src, const uint32_t n, LaneState<V> &st)
 {
     const uint32_t am = __ballot_sync(0xFFFFFFFFu, n > 0);
     const uint32_t cnt = __popc(am), rk = __popc(am & C.lt);
@@ -604,23 +607,26 @@ __device__ __forceinline__ void report(const KernelArgs &a, const Ctx &C, bool o
     }
 }
 
-template <typename V, bool kDecode, bool kHasY, class Src>
+// One slice of a staged chunk: y (or decode positions) from global memory,
+// everything else from shared memory.
+template <typename V, bool kDecode, bool kHasY, bool kDIn>
 __device__ __forceinline__ void decode_slice(const KernelArgs &a, const Ctx &C, const V *__restrict__ x,
-                                             Src src, const uint32_t end, const uint32_t n,
-                                             const uint32_t row, const bool inrow, const int lane)
+                                             const SmemSrc src, const uint32_t end, const uint32_t n,
+                                             const uint32_t row, const int lane)
 {
     using T = ValueTraits<V>;
+    const bool inrow = row < (uint32_t)a.rows;
     const uint32_t maxn = __reduce_max_sync(0xFFFFFFFFu, n);
     const uint32_t max_nseg = (maxn + 7u) >> 3;
-    if (max_nseg > a.long_seg) return;  // task-decoded slice (uniform)
-    const uint32_t orow = (a.row_map != nullptr && inrow) ? __ldg(a.row_map + row) : row;
+    uint32_t orow = row;
+    if (a.row_map != nullptr && inrow) orow = __ldg(a.row_map + row);
     V yv = V(0);
-    if (kHasY) yv = __ldg(reinterpret_cast<const V *>(a.y) + (inrow ? orow : 0u));
+    if (kHasY && inrow) yv = __ldg(reinterpret_cast<const V *>(a.y) + orow);
     LaneState<V> st;
     st.out_pos = 0;
     if (kDecode && inrow) st.out_pos = __ldg(a.row_start + row);
     init_state<V>(C, src, n, st);
-    const bool ok = decode_range<V, kDecode>(a, C, x, src, end, n, maxn, 0u, max_nseg, st, lane);
+    const bool ok = decode_range<V, kDecode, kDIn>(a, C, x, src, end, n, maxn, 0u, max_nseg, st, lane);
     report(a, C, ok, st.cur, end, n, st.col, lane);
     if (!kDecode && inrow) {
         const V res = kHasY ? T::add(st.acc, yv) : st.acc;
@@ -628,34 +634,145 @@ __device__ __forceinline__ void decode_slice(const KernelArgs &a, const Ctx &C, 
     }
 }
 
+__device__ __forceinline__ void st_shared_v2(uint32_t addr, uint32_t x, uint32_t y)
+{
+    asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(addr), "r"(x), "r"(y) : "memory");
+}
+__device__ __forceinline__ uint2 ld_shared_v2(uint32_t addr)
+{
+    uint2 v;
+    asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(addr) : "memory");
+    return v;
+}
+
+// Chunk staging (lane 0): one cp.async.bulk of the chunk's blob completing
+// on the buffer's mbarrier.  The previous contents were consumed by this
+// warp's LDS before the __syncwarp that precedes the call (the same WAR
+// ordering a CUTLASS TMA pipeline relies on), so no proxy fence is issued.
+// All addresses are shared-window addresses.
+__device__ __forceinline__ void stage_chunk(const KernelArgs &a, const bool valid, const ChunkRec rc,
+                                            const uint32_t bar, const uint32_t meta, const uint32_t buf)
+{
+    if (!valid) {
+        st_shared_v2(meta, 0u, 0u);
+        mbar_arrive(bar);
+        return;
+    }
+    const uint32_t bytes = (rc.kw >> 8) * 4u;
+    st_shared_v2(meta, rc.s0, rc.kw & 0xFFu);
+    mbar_arrive_expect_tx(bar, bytes);
+    bulk_g2s(buf, a.blob + rc.off, bytes, bar);
+}
+
+// Per-warp control block of lane 0's claim pipeline (shared memory, so the
+// other 31 lanes do not carry it in registers): the record of the next
+// chunk to stage and the ticket of the one after.
+struct WarpCtl {
+    ChunkRec pend;
+    uint32_t pend_c, next_static, pend_ok, pad;
+};
+
+// Persistent kernel, one CTA of 32 warps per SM: tables -> shared memory once,
+// then every warp walks chunks (static stride or atomic tickets) through its
+// TMA ring.
+template <typename V, bool kDecode, bool kHasY, bool kDIn>
+__global__ void __launch_bounds__(kMaxWarps * 32, 1) dtans_kernel(const KernelArgs a)
+{
+    constexpr int kWarps = kMaxWarps;
+    const bool aligned = load_tables(a);
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    const uint32_t sb = smem_u32(dtans_smem);
+    const uint32_t bars = sb + (uint32_t)a.off_bars + (uint32_t)warp * kMaxRing * 8u;
+    const uint32_t metas = sb + (uint32_t)a.off_meta + (uint32_t)warp * kMaxRing * 8u;
+    WarpCtl *ctl = reinterpret_cast<WarpCtl *>(dtans_smem + a.off_ctl) + warp;
+    if (lane == 0) {
+        for (int b = 0; b < a.nring; b++) mbar_init(bars + 8u * b, 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    if (!aligned) {  // shared-window layout assumption broken: fail loudly
+        if (threadIdx.x == 0) atomicOr(a.err, 4u);
+        return;
+    }
+    const Ctx C = make_ctx<V>(a, lane);
+    const V *__restrict__ x = reinterpret_cast<const V *>(a.x);
+
+    // lane 0's claim pipeline: ticket -> chunk record -> staged buffer
+    auto claim = [&]() -> uint32_t {  // lane 0 only; >= chunk_hi: none
+        if (a.dynamic) return a.chunk_lo + atomicAdd(a.work_counter, 1u);
+        const uint32_t c = ctl->next_static;
+        ctl->next_static = c + gridDim.x * kWarps;
+        return c;
+    };
+    if (lane == 0) {
+        ctl->next_static = a.chunk_lo + blockIdx.x * kWarps + warp;
+        const uint32_t bufs = sb + (uint32_t)a.off_bufs + (uint32_t)warp * (uint32_t)a.nring * (uint32_t)a.bufb;
+        for (int b = 0; b < a.nring; b++) {
+            const uint32_t c = claim();
+            const bool v = c < a.chunk_hi;
+            ChunkRec rc{};
+            if (v) rc = a.chunks[c];
+            stage_chunk(a, v, rc, bars + 8u * b, metas + 8u * b, bufs + b * (uint32_t)a.bufb);
+        }
+        const uint32_t c = claim();
+        ctl->pend_ok = c < a.chunk_hi;
+        if (c < a.chunk_hi) ctl->pend = a.chunks[c];
+        ctl->pend_c = claim();
+    }
+    __syncwarp();
+    uint32_t b = 0, parity = 0;
+    for (;;) {
+        mbar_wait(bars + 8u * b, parity);
+        const uint2 md = ld_shared_v2(metas + 8u * b);
+        const uint32_t s0 = md.x, k = md.y;
+        if (k == 0) break;  // uniform: this warp's chunks are exhausted
+        const uint32_t buf =
+            sb + (uint32_t)a.off_bufs + ((uint32_t)warp * (uint32_t)a.nring + b) * (uint32_t)a.bufb;
+        const uint32_t hw = chunk_hdr_words(k);
+        const uint32_t rs = buf + hw * 4u + (uint32_t)lane * 4u;
+        const uint32_t st = buf + (hw + k * 32u) * 4u;
+        uint32_t dcur = 0;
+        for (uint32_t i = 0; i < k; i++) {
+            const uint32_t dnext = sh32(buf + 4u * (i + 1u));
+            const uint32_t n = sh32(rs + i * 128u);
+            const SmemSrc src{st + dcur * 4u};
+            decode_slice<V, kDecode, kHasY, kDIn>(a, C, x, src, dnext - dcur, n,
+                                                   (s0 + i) * kSliceRows + (uint32_t)lane, lane);
+            dcur = dnext;
+        }
+        __syncwarp();
+        if (lane == 0) {
+            stage_chunk(a, ctl->pend_ok != 0u, ctl->pend, bars + 8u * b, metas + 8u * b, buf);
+            const uint32_t c = ctl->pend_c;
+            ctl->pend_ok = c < a.chunk_hi;
+            if (c < a.chunk_hi) ctl->pend = a.chunks[c];
+            ctl->pend_c = claim();
+        }
+        __syncwarp();
+        if (++b == (uint32_t)a.nring) {
+            b = 0;
+            parity ^= 1u;
+        }
+    }
+}
+
 // Long-slice tasks: each warp decodes segments [j0, j1) of one slice from a
 // checkpoint (or the init events), reading the stream from global memory,
 // and writes its 32 per-lane partial sums (or, when decoding, the columns
 // and value bits of those segments directly).
-template <typename V, bool kDecode>
+template <typename V, bool kDecode, bool kDIn>
 __global__ void __launch_bounds__(512, 2) dtans_task_kernel(const KernelArgs a)
 {
-    using Bits = typename ValueTraits<V>::Bits;
-    extern __shared__ __align__(128) unsigned char smem[];
-    {
-        const int4 *srcv = reinterpret_cast<const int4 *>(a.tables);
-        int4 *dst = reinterpret_cast<int4 *>(smem);
-        for (int i = threadIdx.x; i < a.table_bytes / 16; i += blockDim.x) dst[i] = __ldg(srcv + i);
-    }
+    const bool aligned = load_tables(a);
     __syncthreads();
-    const uint32_t sbase = smem_u32(smem);
-    Ctx C;
-    C.dtab = sbase;
-    C.vtab = sbase + kSlots * 4;
-    C.ddict = sbase + (uint32_t)a.off_ddict;
-    C.vdict = sbase + (uint32_t)a.off_vdict;
-    C.desc_min = a.desc_min;
-    C.vesc_min = a.vesc_min;
-    C.cols_m1 = (uint32_t)(a.cols - 1);
-    C.lt = lanemask_lt();
-    C.pads_ok = a.pads_ok != 0;
-    const V *__restrict__ x = reinterpret_cast<const V *>(a.x);
+    if (!aligned) {
+        if (threadIdx.x == 0) atomicOr(a.err, 4u);
+        return;
+    }
     const int lane = threadIdx.x & 31;
+    const Ctx C = make_ctx<V>(a, lane);
+    const V *__restrict__ x = reinterpret_cast<const V *>(a.x);
     const uint32_t warp = threadIdx.x >> 5;
     const uint32_t warps = blockDim.x >> 5;
     for (uint32_t t = blockIdx.x * warps + warp; t < a.ntasks; t += gridDim.x * warps) {
@@ -665,7 +782,7 @@ __global__ void __launch_bounds__(512, 2) dtans_task_kernel(const KernelArgs a)
         const uint32_t n = inrow ? __ldg(a.row_symbols + row) : 0u;
         const uint32_t maxn = __reduce_max_sync(0xFFFFFFFFu, n);
         const uint64_t lo = __ldg(a.directory + tk.slice);
-        GmemSrc src{a.stream + lo};
+        const GmemSrc src{a.stream + lo};
         LaneState<V> st;
         st.out_pos = 0;
         if (tk.ck == 0xFFFFFFFFu) {
@@ -685,7 +802,7 @@ __global__ void __launch_bounds__(512, 2) dtans_task_kernel(const KernelArgs a)
         }
         // decoding: every segment before j0 of an active lane was full (4 pairs)
         if (kDecode && inrow) st.out_pos = __ldg(a.row_start + row) + 4ll * tk.j0;
-        const bool ok = decode_range<V, kDecode>(a, C, x, src, tk.cur1, n, maxn, tk.j0, tk.j1, st, lane);
+        const bool ok = decode_range<V, kDecode, kDIn>(a, C, x, src, tk.cur1, n, maxn, tk.j0, tk.j1, st, lane);
         report(a, C, ok, st.cur, tk.cur1, tk.last ? n : 0u, st.col, lane);
         if (!kDecode) {
             if (tk.last && tk.j0 == 0) {
@@ -708,21 +825,18 @@ __global__ void __launch_bounds__(512, 2) dtans_task_kernel(const KernelArgs a)
 // slice belongs to that row (container.py:406-413 with one lane), so its
 // words are consecutive from cur0 and the lockstep ballots reduce to a
 // running cursor; 32 independent chunks share a warp.
-template <typename V, bool kDecode>
+template <typename V, bool kDecode, bool kDIn>
 __global__ void __launch_bounds__(256) dtans_solo_kernel(const KernelArgs a)
 {
     using T = ValueTraits<V>;
     using Bits = typename T::Bits;
-    extern __shared__ __align__(128) unsigned char smem[];
-    {
-        const int4 *srcv = reinterpret_cast<const int4 *>(a.tables);
-        int4 *dst = reinterpret_cast<int4 *>(smem);
-        for (int i = threadIdx.x; i < a.table_bytes / 16; i += blockDim.x) dst[i] = __ldg(srcv + i);
-    }
+    const bool aligned = load_tables(a);
     __syncthreads();
-    const uint32_t sbase = smem_u32(smem);
-    const uint32_t dtab = sbase, vtab = sbase + kSlots * 4;
-    const uint32_t ddict = sbase + (uint32_t)a.off_ddict, vdict = sbase + (uint32_t)a.off_vdict;
+    if (!aligned) {
+        if (threadIdx.x == 0) atomicOr(a.err, 4u);
+        return;
+    }
+    const Ctx C = make_ctx<V>(a, (int)(threadIdx.x & 31));
     const uint32_t cols_m1 = (uint32_t)(a.cols - 1);
     const V *__restrict__ x = reinterpret_cast<const V *>(a.x);
     for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < a.nsolo; t += gridDim.x * blockDim.x) {
@@ -740,14 +854,10 @@ __global__ void __launch_bounds__(256) dtans_solo_kernel(const KernelArgs a)
         for (uint32_t j = tk.j0; j < tk.j1; j++) {
             uint32_t so[8], e[8], ds[4];
             Bits vs[4];
-            slot_offsets(w0, w1, w2, so);
+            slot_offsets(C.tab, w0, w1, w2, so);
 #pragma unroll
-            for (int p = 0; p < 4; p++) {
-                e[2 * p] = lds32(dtab + so[2 * p]);
-                e[2 * p + 1] = lds32(vtab + so[2 * p + 1]);
-                ds[p] = lds32(ddict + (e[2 * p] >> 16));
-                vs[p] = lds_bits<Bits>(vdict + (e[2 * p + 1] >> 16));
-            }
+            for (int p = 0; p < 4; p++)
+                lookup_pair<Bits, kDIn>(C, so[2 * p], so[2 * p + 1], e[2 * p], e[2 * p + 1], ds[p], vs[p]);
 #pragma unroll
             for (int p = 0; p < 4; p++) {  // payloads in slot order, low word first
                 if (e[2 * p] >= a.desc_min) ds[p] = __ldg(st + cur++);
@@ -862,159 +972,6 @@ __global__ void __launch_bounds__(256) dtans_finalize_kernel(const KernelArgs a)
 #pragma unroll
         for (int q = 1; q < 8; q++) s = T::add(s, red[q][lane]);
         finish(ls, s);
-    }
-}
-
-
-// Persistent kernel, one CTA of 32 warps per SM: tables -> shared memory once,
-// then every warp walks its slices (grid-wide stride) through its TMA ring.
-template <typename V, bool kDecode, bool kHasY, bool kDyn, int kThreads>
-__global__ void __launch_bounds__(kThreads, 1) dtans_kernel(const KernelArgs a)
-{
-    constexpr int kWarps = kThreads / 32;
-    extern __shared__ __align__(128) unsigned char smem[];
-    {
-        const int4 *srcv = reinterpret_cast<const int4 *>(a.tables);
-        int4 *dst = reinterpret_cast<int4 *>(smem);
-        for (int i = threadIdx.x; i < a.table_bytes / 16; i += blockDim.x) dst[i] = __ldg(srcv + i);
-    }
-    const uint32_t sbase = smem_u32(smem);
-    Ctx C;
-    C.dtab = sbase;
-    C.vtab = sbase + kSlots * 4;
-    C.ddict = sbase + (uint32_t)a.off_ddict;
-    C.vdict = sbase + (uint32_t)a.off_vdict;
-    C.desc_min = a.desc_min;
-    C.vesc_min = a.vesc_min;
-    C.cols_m1 = (uint32_t)(a.cols - 1);
-    C.lt = lanemask_lt();
-    C.pads_ok = a.pads_ok != 0;
-    const V *__restrict__ x = reinterpret_cast<const V *>(a.x);
-    const int lane = threadIdx.x & 31;
-    const int warp = threadIdx.x >> 5;
-    uint64_t *bars = reinterpret_cast<uint64_t *>(smem + a.off_bars) + warp * kRing;
-    SliceMeta *meta = reinterpret_cast<SliceMeta *>(smem + a.off_meta) + warp * kRing;
-    uint32_t *bufs = reinterpret_cast<uint32_t *>(smem + a.off_bufs) + (size_t)warp * kRing * a.bufw;
-    if (lane == 0) {
-        for (int b = 0; b < kRing; b++) mbar_init(&bars[b], 1);
-        fence_mbar_init();
-    }
-    __syncthreads();
-
-    const uint32_t rows = (uint32_t)a.rows;  // < 2^32 (checked at upload)
-    const uint32_t stride = gridDim.x * kWarps;
-    if constexpr (!kDyn) {
-        const uint32_t nsl = a.slice_hi;
-        const uint32_t first = a.slice_lo + blockIdx.x * kWarps + warp;
-        // static order: slices first, first + stride, ...
-        if (lane == 0)
-            for (int b = 0; b < kRing; b++) {
-                const uint32_t s = first + b * stride;
-                if (s < nsl)
-                    stage_slice(a, s, __ldg(a.directory + s), __ldg(a.directory + s + 1), &bars[b], &meta[b],
-                                bufs + b * a.bufw);
-            }
-        uint32_t n_next = 0;
-        if (first < nsl && first * kSliceRows + lane < rows)
-            n_next = __ldg(a.row_symbols + first * kSliceRows + lane);
-        int b = 0;
-        uint32_t parity = 0;
-        for (uint32_t s = first; s < nsl; s += stride) {
-            const uint32_t n = n_next;
-            const uint32_t sn = s + stride;
-            n_next = (sn < nsl && sn * kSliceRows + lane < rows) ? __ldg(a.row_symbols + sn * kSliceRows + lane) : 0u;
-            // directory entries of the slice this buffer is refilled with
-            const uint32_t sr = s + kRing * stride;
-            uint64_t rlo = 0, rhi = 0;
-            if (lane == 0 && sr < nsl) {
-                rlo = __ldg(a.directory + sr);
-                rhi = __ldg(a.directory + sr + 1);
-            }
-            mbar_wait(&bars[b], parity);
-            const SliceMeta md = meta[b];
-            const uint32_t row = s * kSliceRows + lane;
-            const bool inrow = row < rows;
-            const uint32_t aw = ((md.off & ~kGlobalSlice) + md.nwords + 3u) & ~3u;  // aligned window
-            if (aw > a.long_words) {
-                // task-decoded slice (checkpoints.cpp criterion)
-            } else if (!(md.off & kGlobalSlice)) {
-                const SmemSrc src{smem_u32(bufs + b * a.bufw) + md.off * 4u};
-                decode_slice<V, kDecode, kHasY>(a, C, x, src, md.nwords, n, row, inrow, lane);
-            } else {
-                const GmemSrc src{a.stream + __ldg(a.directory + s)};
-                decode_slice<V, kDecode, kHasY>(a, C, x, src, md.nwords, n, row, inrow, lane);
-            }
-            __syncwarp();
-            if (lane == 0 && sr < nsl) stage_slice(a, sr, rlo, rhi, &bars[b], &meta[b], bufs + b * a.bufw);
-            if (++b == kRing) {
-                b = 0;
-                parity ^= 1u;
-            }
-        }
-        return;
-    }
-    const uint32_t nsl = (uint32_t)a.nslices;
-    // Dynamic order (skewed containers): each claim takes the next ticket of
-    // a global counter, in the longest-first order of a.slice_order; tickets
-    // are claimed kRing slices before they are decoded, so the atomic's
-    // latency is hidden.
-    auto claim = [&]() -> uint32_t {  // lane 0 only
-        const uint32_t p = atomicAdd(a.work_counter, 1u);
-        if (p >= nsl) return kNoSlice;
-        return a.slice_order != nullptr ? __ldg(a.slice_order + p) : p;
-    };
-    if (lane == 0) {
-        for (int b = 0; b < kRing; b++) {
-            const uint32_t s = claim();
-            const uint64_t lo = s != kNoSlice ? __ldg(a.directory + s) : 0, hi = s != kNoSlice ? __ldg(a.directory + s + 1) : 0;
-            stage_slice(a, s, lo, hi, &bars[b], &meta[b], bufs + b * a.bufw);
-        }
-    }
-    __syncwarp();
-    uint32_t s_next = meta[0].slice;
-    uint32_t n_next = (s_next != kNoSlice && s_next * kSliceRows + lane < rows)
-                          ? __ldg(a.row_symbols + s_next * kSliceRows + lane)
-                          : 0u;
-    int b = 0;
-    uint32_t parity = 0;
-    for (;;) {
-        // claim the slice this buffer is refilled with, prefetch its directory entries
-        uint32_t sr = kNoSlice;
-        uint64_t rlo = 0, rhi = 0;
-        if (lane == 0) {
-            sr = claim();
-            if (sr != kNoSlice) {
-                rlo = __ldg(a.directory + sr);
-                rhi = __ldg(a.directory + sr + 1);
-            }
-        }
-        mbar_wait(&bars[b], parity);
-        const SliceMeta md = meta[b];
-        const uint32_t s = md.slice;
-        if (s == kNoSlice) break;  // uniform
-        const uint32_t n = n_next;
-        const int bn = b + 1 == kRing ? 0 : b + 1;
-        s_next = meta[bn].slice;
-        n_next = (s_next != kNoSlice && s_next * kSliceRows + lane < rows)
-                     ? __ldg(a.row_symbols + s_next * kSliceRows + lane)
-                     : 0u;
-        const uint32_t row = s * kSliceRows + lane;
-        const bool inrow = row < rows;
-        const uint32_t aw = ((md.off & ~kGlobalSlice) + md.nwords + 3u) & ~3u;  // aligned window
-        if (aw > a.long_words) {
-            // task-decoded slice (checkpoints.cpp criterion)
-        } else if (!(md.off & kGlobalSlice)) {
-            const SmemSrc src{smem_u32(bufs + b * a.bufw) + md.off * 4u};
-            decode_slice<V, kDecode, kHasY>(a, C, x, src, md.nwords, n, row, inrow, lane);
-        } else {
-            const GmemSrc src{a.stream + __ldg(a.directory + s)};
-            decode_slice<V, kDecode, kHasY>(a, C, x, src, md.nwords, n, row, inrow, lane);
-        }
-        __syncwarp();
-        if (lane == 0) stage_slice(a, sr, rlo, rhi, &bars[b], &meta[b], bufs + b * a.bufw);
-        __syncwarp();
-        b = bn;
-        if (b == 0) parity ^= 1u;
     }
 }
 
