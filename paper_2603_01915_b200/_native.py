@@ -14,7 +14,7 @@ import os
 from .errors import CodingError, CorruptStream, NativeUnavailable, ParameterError
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libdtans.so")
+LIB_PATH = os.environ.get("DTANS_LIB") or os.path.join(HERE, "libdtans.so")  # DTANS_LIB: experiment builds
 
 DTANS_OK, DTANS_E_PARAM, DTANS_E_CODING, DTANS_E_CORRUPT = 0, 1, 2, 3
 DTANS_E_CUDA, DTANS_E_NOMEM, DTANS_E_NODEVICE = 4, 5, 6

@@ -434,14 +434,10 @@ extern "C" int dtans_upload(const dtans_container_view *c, int device, dtans_dev
             m = std::max(m, c->row_symbols[i]);
         cost[s] = (m + 7) / 8;
     }
-    // staging ring: 3 buffers per warp unless the largest (non-long) slice
-    // only fits with 2
-    uint64_t max_single = 0;
-    for (int64_t s = 0; s < nsl; s++)
-        if (cost[s] <= (uint32_t)long_seg) max_single = std::max(max_single, chunk_bytes(c->directory, s, 1));
-    SmemPlan sp = plan_smem(tb, max_optin, 3);
+    // staging ring: 2 buffers per warp (measured: larger chunks beat a
+    // deeper ring; 32 warps x 2 chunks in flight cover the HBM latency)
     const char *er = getenv("DTANS_RING");
-    if (er ? atoi(er) == 2 : max_single > (uint64_t)sp.bufb) sp = plan_smem(tb, max_optin, 2);
+    SmemPlan sp = plan_smem(tb, max_optin, er ? std::max(2, std::min(3, atoi(er))) : 2);
     if (sp.bufb < 512) {
         delete h;
         return fail(DTANS_E_CUDA, "coding tables leave no shared memory for staging");

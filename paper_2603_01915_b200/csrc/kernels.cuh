@@ -305,40 +305,71 @@ __device__ __forceinline__ void lookup_pair(const Ctx &C, uint32_t sod, uint32_t
 
 // Payload event (container.py:459-470): per-lane word counts, exclusive warp
 // scan, words read in slot order, low word first, overwriting the symbols.
-template <typename T, class Src>
-__device__ __forceinline__ void payload_event(const Ctx &C, const Src &src, uint32_t &cur, const bool act,
-                                              const uint32_t e[8], uint32_t ds[4], typename T::Bits vs[4])
+// Split in three so callers can give the general (slow) case its own copy
+// of the rest of the segment: the common paths then never merge 64-bit value
+// registers (no register shuffling on the hot path).
+//   payload_probe: 0 = no escape in the warp, 1 = fast case (every lane needs
+//   at most one payload word: its rank among the escaping lanes; f64 value
+//   escapes never qualify), 2 = general case.
+template <typename T>
+__device__ __forceinline__ int payload_probe(const Ctx &C, const bool act, const uint32_t e[8])
 {
-    using Bits = typename T::Bits;
+    const uint32_t FULL = 0xFFFFFFFFu;
     // cheap test first: escape entries are the largest entries of a table
     const uint32_t dmax = max(max(e[0], e[2]), max(e[4], e[6]));
     const uint32_t vmax = max(max(e[1], e[3]), max(e[5], e[7]));
-    const bool has = act && (dmax >= C.desc_min || vmax >= C.vesc_min);
-    if (!__any_sync(0xFFFFFFFFu, has)) return;
+    const bool dany = act && dmax >= C.desc_min;
+    const bool vany = act && vmax >= C.vesc_min;
+    if (!__any_sync(FULL, dany || vany)) return 0;
+    const bool d0 = e[0] >= C.desc_min, d1 = e[2] >= C.desc_min, d2 = e[4] >= C.desc_min, d3 = e[6] >= C.desc_min;
+    const bool dmulti = (d0 && (d1 || d2 || d3)) || (d1 && (d2 || d3)) || (d2 && d3);
+    bool fast;
+    if (T::kPayloadWords == 2) {
+        fast = !vany && !dmulti;
+    } else {
+        const bool v0 = e[1] >= C.vesc_min, v1 = e[3] >= C.vesc_min, v2 = e[5] >= C.vesc_min,
+                   v3 = e[7] >= C.vesc_min;
+        const bool vmulti = (v0 && (v1 || v2 || v3)) || (v1 && (v2 || v3)) || (v2 && v3);
+        fast = !(dmulti || vmulti || (dany && vany));
+    }
+    return __all_sync(FULL, !act || fast) ? 1 : 2;
+}
+
+template <typename T, class Src>
+__device__ __forceinline__ void payload_fast(const Ctx &C, const Src &src, uint32_t &cur, const bool act,
+                                             const uint32_t e[8], uint32_t ds[4], typename T::Bits vs[4])
+{
+    using Bits = typename T::Bits;
+    bool esc = false;
+#pragma unroll
+    for (int k = 0; k < 8; k++) esc = esc || e[k] >= ((k & 1) ? C.vesc_min : C.desc_min);
+    const uint32_t m = __ballot_sync(0xFFFFFFFFu, act && esc);
+    const uint32_t w = src(cur + __popc(m & C.lt));
+    cur += __popc(m);
+#pragma unroll
+    for (int p = 0; p < 4; p++) {
+        if (e[2 * p] >= C.desc_min) ds[p] = w;
+        if (T::kPayloadWords == 1 && e[2 * p + 1] >= C.vesc_min) vs[p] = (Bits)w;
+    }
+}
+
+template <typename T, class Src>
+__device__ __forceinline__ void payload_slow(const Ctx &C, const Src &src, uint32_t &cur, const bool act,
+                                             const uint32_t e[8], uint32_t ds[4], typename T::Bits vs[4])
+{
+    using Bits = typename T::Bits;
+    const uint32_t FULL = 0xFFFFFFFFu;
     uint32_t pc = 0;
 #pragma unroll
     for (int p = 0; p < 4; p++)
         pc += (e[2 * p] >= C.desc_min ? 1u : 0u) + (e[2 * p + 1] >= C.vesc_min ? (uint32_t)T::kPayloadWords : 0u);
     if (!act) pc = 0;
-    const uint32_t any = __ballot_sync(0xFFFFFFFFu, pc != 0);
-    if (__all_sync(0xFFFFFFFFu, pc <= 1u)) {
-        // common case (e.g. one escaped first column per row): every lane
-        // reads at most one word, its rank among the escaping lanes
-        const uint32_t w = src(cur + __popc(any & C.lt));
-#pragma unroll
-        for (int p = 0; p < 4; p++) {
-            if (e[2 * p] >= C.desc_min) ds[p] = w;
-            if (T::kPayloadWords == 1 && e[2 * p + 1] >= C.vesc_min) vs[p] = (Bits)w;
-        }
-        cur += __popc(any);
-        return;
-    }
     // exclusive warp scan of pc (<= 12 words: 4 bit planes), one ballot per
     // plane: independent ballots instead of a dependent 5-step shuffle chain
-    const uint32_t b1 = __ballot_sync(0xFFFFFFFFu, pc & 2u);
-    const uint32_t b2 = __ballot_sync(0xFFFFFFFFu, pc & 4u);
-    const uint32_t b3 = __ballot_sync(0xFFFFFFFFu, pc & 8u);
-    const uint32_t b0 = __ballot_sync(0xFFFFFFFFu, pc & 1u);
+    const uint32_t b1 = __ballot_sync(FULL, pc & 2u);
+    const uint32_t b2 = __ballot_sync(FULL, pc & 4u);
+    const uint32_t b3 = __ballot_sync(FULL, pc & 8u);
+    const uint32_t b0 = __ballot_sync(FULL, pc & 1u);
     const uint32_t excl = __popc(b0 & C.lt) + (__popc(b1 & C.lt) << 1) + (__popc(b2 & C.lt) << 2) +
                           (__popc(b3 & C.lt) << 3);
     const uint32_t total = __popc(b0) + (__popc(b1) << 1) + (__popc(b2) << 2) + (__popc(b3) << 3);
@@ -362,6 +393,17 @@ __device__ __forceinline__ void payload_event(const Ctx &C, const Src &src, uint
         }
     }
     cur += total;
+}
+
+// All three in one (final segments and the solo path, where the extra
+// copy is not worth it).
+template <typename T, class Src>
+__device__ __forceinline__ void payload_event(const Ctx &C, const Src &src, uint32_t &cur, const bool act,
+                                              const uint32_t e[8], uint32_t ds[4], typename T::Bits vs[4])
+{
+    const int pk = payload_probe<T>(C, act, e);
+    if (pk == 1) payload_fast<T>(C, src, cur, act, e, ds, vs);
+    else if (pk == 2) payload_slow<T>(C, src, cur, act, e, ds, vs);
 }
 
 __device__ __forceinline__ uint32_t byte1(uint32_t x) { return __byte_perm(x, 0u, 0x4441u); }
@@ -424,59 +466,69 @@ __device__ __forceinline__ void full_segment(const KernelArgs &a, const Ctx &C, 
 #pragma unroll
     for (int p = 0; p < 4; p++)
         lookup_pair<Bits, kDIn>(C, so[2 * p], so[2 * p + 1], e[2 * p], e[2 * p + 1], ds[p], vs[p]);
-    payload_event<T>(C, src, cur, act, e, ds, vs);
-    V xv[4];
-#pragma unroll
-    for (int p = 0; p < 4; p++) {
-        const bool valid = kHot || 8u * j + 2u * p < n;
-        xv[p] = V(0);
-        if (valid) {
-            col += ds[p];
-            if (kDecode) {
-                a.dec_cols[out_pos] = (int64_t)col;
-                reinterpret_cast<Bits *>(a.dec_vals)[out_pos] = vs[p];
-                out_pos++;
-            } else {
-                xv[p] = __ldg(x + min(col, C.cols_m1));
-            }
-        }
-    }
-    // mixed-radix checks (container.py:478-497): bases decide load vs extract
-    uint32_t bm1a, dga, bm1b, dgb;
-    group(e[0], e[1], e[2], e[3], bm1a, dga);
-    group(e[4], e[5], e[6], e[7], bm1b, dgb);
-    uint32_t r1l, r1h, r2l, r2h;
-    mad_wide(r, bm1a, r, 0u, r1l, r1h);
-    const bool ext0 = r1h != 0u;
-    const uint32_t ra = ext0 ? r1h : r1l;
-    mad_wide(ra, bm1b, ra, 0u, r2l, r2h);
-    const bool ext1 = r2h != 0u;
-    const uint32_t m_ld0 = __ballot_sync(FULL, notlast && !ext0);
-    const uint32_t m_ld1 = __ballot_sync(FULL, notlast && !ext1);
-    const uint32_t m_nl = kHot ? FULL : __ballot_sync(FULL, notlast);
-    const uint32_t c1 = cur + __popc(m_ld0);
-    const uint32_t c2 = c1 + __popc(m_ld1);
-    const uint32_t lw0 = src(cur + __popc(m_ld0 & C.lt));
-    const uint32_t lw1 = src(c1 + __popc(m_ld1 & C.lt));
-    const uint32_t lw2 = src(c2 + (kHot ? (uint32_t)lane : __popc(m_nl & C.lt)));
-    cur = c2 + (kHot ? 32u : __popc(m_nl));
-    if (notlast) {
-        uint32_t d1l, d1h, d2l, d2h;
-        fold(d, bm1a, dga, d1l, d1h);
-        const uint32_t da = ext0 ? d1h : d1l;
-        w0 = ext0 ? d1l : lw0;
-        fold(da, bm1b, dgb, d2l, d2h);
-        w1 = ext1 ? d2l : lw1;
-        d = ext1 ? d2h : d2l;
-        r = ext1 ? r2h : r2l;
-        w2 = lw2;
-    }
-    if (!kDecode) {
+    // the rest of the segment once the symbols are final
+    auto rest = [&](const uint32_t (&ds)[4], const Bits (&vs)[4]) __attribute__((always_inline)) {
+        V xv[4];
 #pragma unroll
         for (int p = 0; p < 4; p++) {
-            if (kHot || 8u * j + 2u * p < n) acc = T::add(acc, T::mul(T::from_bits(vs[p]), xv[p]));
+            const bool valid = kHot || 8u * j + 2u * p < n;
+            xv[p] = V(0);
+            if (valid) {
+                col += ds[p];
+                if (kDecode) {
+                    a.dec_cols[out_pos] = (int64_t)col;
+                    reinterpret_cast<Bits *>(a.dec_vals)[out_pos] = vs[p];
+                    out_pos++;
+                } else {
+                    xv[p] = __ldg(x + min(col, C.cols_m1));
+                }
+            }
         }
+        // mixed-radix checks (container.py:478-497): bases decide load vs extract
+        uint32_t bm1a, dga, bm1b, dgb;
+        group(e[0], e[1], e[2], e[3], bm1a, dga);
+        group(e[4], e[5], e[6], e[7], bm1b, dgb);
+        uint32_t r1l, r1h, r2l, r2h;
+        mad_wide(r, bm1a, r, 0u, r1l, r1h);
+        const bool ext0 = r1h != 0u;
+        const uint32_t ra = ext0 ? r1h : r1l;
+        mad_wide(ra, bm1b, ra, 0u, r2l, r2h);
+        const bool ext1 = r2h != 0u;
+        const uint32_t m_ld0 = __ballot_sync(FULL, notlast && !ext0);
+        const uint32_t m_ld1 = __ballot_sync(FULL, notlast && !ext1);
+        const uint32_t m_nl = kHot ? FULL : __ballot_sync(FULL, notlast);
+        const uint32_t c1 = cur + __popc(m_ld0);
+        const uint32_t c2 = c1 + __popc(m_ld1);
+        const uint32_t lw0 = src(cur + __popc(m_ld0 & C.lt));
+        const uint32_t lw1 = src(c1 + __popc(m_ld1 & C.lt));
+        const uint32_t lw2 = src(c2 + (kHot ? (uint32_t)lane : __popc(m_nl & C.lt)));
+        cur = c2 + (kHot ? 32u : __popc(m_nl));
+        if (notlast) {
+            uint32_t d1l, d1h, d2l, d2h;
+            fold(d, bm1a, dga, d1l, d1h);
+            const uint32_t da = ext0 ? d1h : d1l;
+            w0 = ext0 ? d1l : lw0;
+            fold(da, bm1b, dgb, d2l, d2h);
+            w1 = ext1 ? d2l : lw1;
+            d = ext1 ? d2h : d2l;
+            r = ext1 ? r2h : r2l;
+            w2 = lw2;
+        }
+        if (!kDecode) {
+#pragma unroll
+            for (int p = 0; p < 4; p++) {
+                if (kHot || 8u * j + 2u * p < n) acc = T::add(acc, T::mul(T::from_bits(vs[p]), xv[p]));
+            }
+        }
+    };
+    const int pk = payload_probe<T>(C, act, e);
+    if (pk == 2) {
+        payload_slow<T>(C, src, cur, act, e, ds, vs);
+        rest(ds, vs);
+        return;
     }
+    if (pk == 1) payload_fast<T>(C, src, cur, act, e, ds, vs);
+    rest(ds, vs);
 }
 
 // Per-lane decoder state carried between segments (and restored from a
