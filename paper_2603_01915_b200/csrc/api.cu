@@ -16,6 +16,7 @@
 using namespace dtans;
 
 constexpr int kHostChunks = 8;
+constexpr size_t kRawStreamPad = dev::kStreamPadWords;
 
 struct dtans_dev {
     int device = 0;
@@ -300,20 +301,20 @@ int configure(dtans_dev *h, const TableBlock &tb, const SmemPlan &sp)
     h->sms = sms;
     if (a.nlong) {
         h->task_smem = (int)align_up((size_t)(a.off_img + a.table_bytes), 16);
-        h->solo_smem = h->task_smem;
+        h->solo_smem = (int)align_up((size_t)(a.off_img + a.table_bytes), 16);
         int per = 0, pers = 0;
         int rc = with_long_kernels<V>(tb.dinline, [&](auto kt, auto ktd, auto ks, auto ksd) -> int {
             CK(cudaFuncSetAttribute(kt, cudaFuncAttributeMaxDynamicSharedMemorySize, h->task_smem), "attr");
             CK(cudaFuncSetAttribute(ktd, cudaFuncAttributeMaxDynamicSharedMemorySize, h->task_smem), "attr");
             CK(cudaFuncSetAttribute(ks, cudaFuncAttributeMaxDynamicSharedMemorySize, h->solo_smem), "attr");
             CK(cudaFuncSetAttribute(ksd, cudaFuncAttributeMaxDynamicSharedMemorySize, h->solo_smem), "attr");
-            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kt, 512, h->task_smem), "occupancy");
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kt, dev::kTaskWarps * 32, h->task_smem), "occupancy");
             CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pers, ks, 256, h->solo_smem), "occupancy");
             return DTANS_OK;
         });
         if (rc) return rc;
         h->task_ctas = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)sms * std::max(per, 1),
-                                                                    ((int64_t)a.ntasks + 15) / 16));
+                                                                    ((int64_t)a.ntasks + dev::kTaskWarps - 1) / dev::kTaskWarps));
         h->solo_ctas = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)sms * std::max(pers, 1),
                                                                     ((int64_t)a.nsolo + 255) / 256));
     }
@@ -367,10 +368,10 @@ int launch(dtans_dev *h, const V *x, const V *y, V *out, const int64_t *row_star
     if (a.nlong && c_lo < 0) {
         with_long_kernels<V>(h->dinline, [&](auto kt, auto ktd, auto ks, auto ksd) -> int {
             if (decode_only) {
-                if (a.ntasks) ktd<<<h->task_ctas, 512, h->task_smem, st>>>(a);
+                if (a.ntasks) ktd<<<h->task_ctas, dev::kTaskWarps * 32, h->task_smem, st>>>(a);
                 if (a.nsolo) ksd<<<h->solo_ctas, 256, h->solo_smem, st>>>(a);
             } else {
-                if (a.ntasks) kt<<<h->task_ctas, 512, h->task_smem, st>>>(a);
+                if (a.ntasks) kt<<<h->task_ctas, dev::kTaskWarps * 32, h->task_smem, st>>>(a);
                 if (a.nsolo) ks<<<h->solo_ctas, 256, h->solo_smem, st>>>(a);
             }
             return 0;
@@ -524,7 +525,7 @@ extern "C" int dtans_upload(const dtans_container_view *c, int device, dtans_dev
     if (need_raw) {
         o_rs = off; off = align_up(off + sizeof(uint32_t) * (size_t)std::max<int64_t>(c->rows, 1), 256);
         o_di = off; off = align_up(off + sizeof(uint64_t) * (size_t)(nsl + 1), 256);
-        o_st = off; off = align_up(off + sizeof(uint32_t) * ((size_t)c->nwords + dev::kStreamPadWords), 256);
+        o_st = off; off = align_up(off + sizeof(uint32_t) * ((size_t)c->nwords + kRawStreamPad), 256);
     }
     cudaError_t e = cudaMalloc(&h->d_base, off);
     if (e != cudaSuccess) {
@@ -584,7 +585,7 @@ extern "C" int dtans_upload(const dtans_container_view *c, int device, dtans_dev
         cp(h->d_row_symbols, c->row_symbols, sizeof(uint32_t) * (size_t)c->rows);
         cp(h->d_directory, c->directory, sizeof(uint64_t) * (size_t)(nsl + 1));
         cp(h->d_stream, c->stream, sizeof(uint32_t) * (size_t)c->nwords);
-        zero(h->d_stream + c->nwords, sizeof(uint32_t) * dev::kStreamPadWords);
+        zero(h->d_stream + c->nwords, sizeof(uint32_t) * kRawStreamPad);
     }
     zero(h->d_err, 64);
     cp(h->d_chunks, h->chunks.data(), sizeof(dev::ChunkRec) * h->chunks.size());
@@ -621,6 +622,12 @@ extern "C" int dtans_upload(const dtans_container_view *c, int device, dtans_dev
         delete h;
         return rc;
     }
+    if (getenv("DTANS_VERBOSE"))
+        fprintf(stderr,
+                "[dtans] rows=%lld slices=%lld chunks=%zu nring=%d bufb=%d smem=%d dinline=%d rep_d=%d rep_v=%d "
+                "nlong=%u ntasks=%u nsolo=%u dynamic=%d task_smem=%d\n",
+                (long long)h->rows, (long long)nsl, h->chunks.size(), sp.nring, sp.bufb, h->smem, (int)tb.dinline,
+                tb.rep_d, tb.rep_v, h->base.nlong, h->base.ntasks, h->base.nsolo, h->base.dynamic, h->task_smem);
     *out = h;
     return DTANS_OK;
 }

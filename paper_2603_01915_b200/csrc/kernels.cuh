@@ -212,6 +212,24 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void *src, uint32_t
         : "memory");
 }
 
+// Streamed container bytes are read exactly once per SpMV: mark them
+// evict-first in L2 so they do not push out x, which is gathered repeatedly.
+__device__ __forceinline__ unsigned long long policy_evict_first()
+{
+    unsigned long long pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ void bulk_g2s_stream(uint32_t dst, const void *src, uint32_t bytes, uint32_t bar)
+{
+    asm volatile(
+        "{\n.reg .b64 pol;\n"
+        "createpolicy.fractional.L2::evict_first.b64 pol, 1.0;\n"
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], pol;\n}"
+        ::"r"(dst), "l"(src), "r"(bytes), "r"(bar)
+        : "memory");
+}
+
 __device__ __forceinline__ void fence_mbar_init()
 {
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -230,10 +248,18 @@ constexpr uint32_t kStreamPadWords = kOverrunWords;  // device stream padding
 struct SmemSrc {
     uint32_t addr;  // shared address of word directory[s]
     __device__ __forceinline__ uint32_t operator()(uint32_t rel) const { return sh32(addr + rel * 4u); }
+    __device__ __forceinline__ void prepare(uint32_t) {}
 };
 struct GmemSrc {
     const uint32_t *p;  // &stream[directory[s]]
-    __device__ __forceinline__ uint32_t operator()(uint32_t rel) const { return __ldg(p + rel); }
+    unsigned long long pol;  // L2 evict-first policy (streamed words)
+    __device__ __forceinline__ uint32_t operator()(uint32_t rel) const
+    {
+        uint32_t v;
+        asm("ld.global.nc.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(p + rel), "l"(pol));
+        return v;
+    }
+    __device__ __forceinline__ void prepare(uint32_t) {}
 };
 
 // Per-lane shared-memory context (absolute shared addresses).  The delta
@@ -590,7 +616,7 @@ __device__ __forceinline__ void final_segment(const KernelArgs &a, const Ctx &C,
 // may escape).  Returns false if the cursor ran past `end` (corrupt slice).
 template <typename V, bool kDecode, bool kDIn, class Src>
 __device__ __forceinline__ bool decode_range(const KernelArgs &a, const Ctx &C, const V *__restrict__ x,
-                                             const Src &src, const uint32_t end, const uint32_t n,
+                                             Src &src, const uint32_t end, const uint32_t n,
                                              const uint32_t maxn, const uint32_t j0, const uint32_t j1,
                                              LaneState<V> &st, const int lane)
 {
@@ -604,11 +630,13 @@ __device__ __forceinline__ bool decode_range(const KernelArgs &a, const Ctx &C, 
     uint32_t j = j0;
     const uint32_t jhot = min(jfull, min_nseg > 0 ? min_nseg - 1u : 0u);
     for (; j < jhot; j++) {
+        src.prepare(st.cur);
         full_segment<V, kDecode, true, kDIn>(a, C, x, src, j, n, nseg, st.w0, st.w1, st.w2, st.d, st.r, st.cur,
                                              st.col, st.acc, st.out_pos, lane);
         if (st.cur > end) return false;  // uniform
     }
     for (; j < jfull; j++) {
+        src.prepare(st.cur);
         full_segment<V, kDecode, false, kDIn>(a, C, x, src, j, n, nseg, st.w0, st.w1, st.w2, st.d, st.r,
                                               st.cur, st.col, st.acc, st.out_pos, lane);
         if (st.cur > end) return false;
@@ -618,6 +646,7 @@ __device__ __forceinline__ bool decode_range(const KernelArgs &a, const Ctx &C, 
         // lookups are needed only when pads may escape (escape-only table)
         const uint32_t jf = max_nseg - 1;
         const uint32_t np = C.pads_ok ? (maxn - 8u * jf) >> 1 : 4u;
+        src.prepare(st.cur);
         switch (np) {  // uniform
         case 1: final_segment<V, kDecode, kDIn, 1>(a, C, x, src, jf, n, st); break;
         case 2: final_segment<V, kDecode, kDIn, 2>(a, C, x, src, jf, n, st); break;
@@ -630,7 +659,7 @@ __device__ __forceinline__ bool decode_range(const KernelArgs &a, const Ctx &C, 
 
 // init events (container.py:426-429): 3 words per active lane
 template <typename V, class Src>
-__device__ __forceinline__ void init_state(const Ctx &C, const Src &src, const uint32_t n, LaneState<V> &st)
+__device__ __forceinline__ void init_state(const Ctx &C, Src &src, const uint32_t n, LaneState<V> &st)
 {
     const uint32_t am = __ballot_sync(0xFFFFFFFFu, n > 0);
     const uint32_t cnt = __popc(am), rk = __popc(am & C.lt);
@@ -663,7 +692,7 @@ __device__ __forceinline__ void report(const KernelArgs &a, const Ctx &C, bool o
 // everything else from shared memory.
 template <typename V, bool kDecode, bool kHasY, bool kDIn>
 __device__ __forceinline__ void decode_slice(const KernelArgs &a, const Ctx &C, const V *__restrict__ x,
-                                             const SmemSrc src, const uint32_t end, const uint32_t n,
+                                             SmemSrc src, const uint32_t end, const uint32_t n,
                                              const uint32_t row, const int lane)
 {
     using T = ValueTraits<V>;
@@ -713,7 +742,7 @@ __device__ __forceinline__ void stage_chunk(const KernelArgs &a, const bool vali
     const uint32_t bytes = (rc.kw >> 8) * 4u;
     st_shared_v2(meta, rc.s0, rc.kw & 0xFFu);
     mbar_arrive_expect_tx(bar, bytes);
-    bulk_g2s(buf, a.blob + rc.off, bytes, bar);
+    bulk_g2s_stream(buf, a.blob + rc.off, bytes, bar);
 }
 
 // Per-warp control block of lane 0's claim pipeline (shared memory, so the
@@ -809,12 +838,14 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) dtans_kernel(const KernelAr
     }
 }
 
+constexpr int kTaskWarps = 16;  // task kernel: 512 threads, 2 CTAs per SM
+
 // Long-slice tasks: each warp decodes segments [j0, j1) of one slice from a
 // checkpoint (or the init events), reading the stream from global memory,
 // and writes its 32 per-lane partial sums (or, when decoding, the columns
 // and value bits of those segments directly).
 template <typename V, bool kDecode, bool kDIn>
-__global__ void __launch_bounds__(512, 2) dtans_task_kernel(const KernelArgs a)
+__global__ void __launch_bounds__(kTaskWarps * 32, 2) dtans_task_kernel(const KernelArgs a)
 {
     const bool aligned = load_tables(a);
     __syncthreads();
@@ -823,18 +854,18 @@ __global__ void __launch_bounds__(512, 2) dtans_task_kernel(const KernelArgs a)
         return;
     }
     const int lane = threadIdx.x & 31;
-    const Ctx C = make_ctx<V>(a, lane);
-    const V *__restrict__ x = reinterpret_cast<const V *>(a.x);
     const uint32_t warp = threadIdx.x >> 5;
     const uint32_t warps = blockDim.x >> 5;
+    const Ctx C = make_ctx<V>(a, lane);
+    const V *__restrict__ x = reinterpret_cast<const V *>(a.x);
+    const unsigned long long pol = policy_evict_first();
     for (uint32_t t = blockIdx.x * warps + warp; t < a.ntasks; t += gridDim.x * warps) {
         const LongTask tk = a.tasks[t];
         const uint32_t row = tk.slice * kSliceRows + lane;
         const bool inrow = row < (uint32_t)a.rows;
         const uint32_t n = inrow ? __ldg(a.row_symbols + row) : 0u;
         const uint32_t maxn = __reduce_max_sync(0xFFFFFFFFu, n);
-        const uint64_t lo = __ldg(a.directory + tk.slice);
-        const GmemSrc src{a.stream + lo};
+        GmemSrc src{a.stream + __ldg(a.directory + tk.slice), pol};
         LaneState<V> st;
         st.out_pos = 0;
         if (tk.ck == 0xFFFFFFFFu) {
