@@ -427,7 +427,7 @@ extern "C" int dtans_upload(const dtans_container_view *c, int device, dtans_dev
 
     // per-slice cost (segments of the longest row) and the long-slice split
     const char *e1 = getenv("DTANS_LONG_SEG"), *e2 = getenv("DTANS_CHUNK");
-    const int long_seg = e1 ? atoi(e1) : 64, chunk = e2 ? atoi(e2) : 32;
+    const int long_seg = e1 ? atoi(e1) : 64, chunk = e2 ? atoi(e2) : 16;
     std::vector<uint32_t> cost((size_t)nsl);
     for (int64_t s = 0; s < nsl; s++) {
         uint32_t m = 0;

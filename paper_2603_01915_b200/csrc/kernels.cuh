@@ -47,6 +47,9 @@ namespace dev {
 
 constexpr int kSliceRows = 32;
 constexpr int kSlots = 4096;
+#ifndef DTANS_TASK_WARPS
+#define DTANS_TASK_WARPS 32
+#endif
 #ifndef DTANS_CTA_WARPS
 #define DTANS_CTA_WARPS 32
 #endif
@@ -838,14 +841,14 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) dtans_kernel(const KernelAr
     }
 }
 
-constexpr int kTaskWarps = 16;  // task kernel: 512 threads, 2 CTAs per SM
+constexpr int kTaskWarps = DTANS_TASK_WARPS;  // task kernel CTA size (warps)
 
 // Long-slice tasks: each warp decodes segments [j0, j1) of one slice from a
 // checkpoint (or the init events), reading the stream from global memory,
 // and writes its 32 per-lane partial sums (or, when decoding, the columns
 // and value bits of those segments directly).
 template <typename V, bool kDecode, bool kDIn>
-__global__ void __launch_bounds__(kTaskWarps * 32, 2) dtans_task_kernel(const KernelArgs a)
+__global__ void __launch_bounds__(kTaskWarps * 32, 1024 / (kTaskWarps * 32)) dtans_task_kernel(const KernelArgs a)
 {
     const bool aligned = load_tables(a);
     __syncthreads();
