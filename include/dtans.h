@@ -125,6 +125,18 @@ int dtans_spmv_f64(dtans_dev *h, const double *x, const double *y, double *out,
 int dtans_spmv_f32(dtans_dev *h, const float *x, const float *y, float *out,
                    void *stream);
 
+/* One power-iteration step fused into the SpMV epilogue (configs[4]; the
+ * reference has no such entry: it replaces the loop body
+ *   y = spmv(c, x, 0); n = ||y||; x = y / n
+ * of a caller iterating the reference spmv, container.py:554-596):
+ *   out = (A x) / sqrt(*sumsq_in)         (no scaling if sumsq_in is NULL)
+ *   *sumsq_out += sum(out^2)              (f64 accumulation, atomic per warp)
+ *   *sumsq_zero = 0                       (the next step's accumulator)
+ * Device pointers; x and out in the container precision; the three scalars
+ * must be distinct.  Containers with long slices are refused (PARAM). */
+int dtans_spmv_scaled(dtans_dev *h, const void *x, void *out, const double *sumsq_in,
+                      double *sumsq_out, double *sumsq_zero, void *stream);
+
 /* Same product with HOST x, y, out (pageable or pinned): H2D copy, kernel,
  * D2H copy, synchronize, consumption check.  The end-to-end entry point a
  * ctypes binding of spmv(c, x, y) calls. */

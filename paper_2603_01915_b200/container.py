@@ -286,6 +286,23 @@ class DeviceContainer:
                          out.data_ptr(), stream))
         return out
 
+    def spmv_scaled(self, x, out, sumsq_in, sumsq_out, sumsq_zero=None, stream=None):
+        """One fused power-iteration step on torch CUDA tensors (asynchronous):
+        out = (A x) / sqrt(sumsq_in) (unscaled if sumsq_in is None),
+        sumsq_out += sum(out^2), sumsq_zero = 0 (f64 device scalars)."""
+        torch = _torch()
+        dt = torch.float64 if self.precision == 8 else torch.float32
+        if x.dtype != dt or x.numel() != self.cols or not x.is_cuda:
+            raise ParameterError("x must be a contiguous CUDA tensor of the container dtype/size")
+        if out.dtype != dt or out.numel() != self.rows or not out.is_cuda:
+            raise ParameterError("out must be a CUDA tensor of the container dtype/size")
+        if stream is None:
+            stream = torch.cuda.current_stream(x.device).cuda_stream
+        ptr = (lambda t: t.data_ptr() if t is not None else None)
+        _native.check(_native.lib().dtans_spmv_scaled(self.handle, x.data_ptr(), out.data_ptr(), ptr(sumsq_in),
+                                                      ptr(sumsq_out), ptr(sumsq_zero), stream))
+        return out
+
     def check(self, stream=None):
         """Synchronize and raise CorruptStream if a kernel flagged the stream."""
         if stream is None:

@@ -240,15 +240,15 @@ uint64_t chunk_words(const uint64_t *dir, int64_t s0, int64_t k)
 }
 uint64_t chunk_bytes(const uint64_t *dir, int64_t s0, int64_t k) { return 4 * chunk_words(dir, s0, k); }
 
-// Dispatch on the delta-dictionary mode.
+// Dispatch on the delta-dictionary mode: (spmv, y-less spmv, decode, scaled y-less spmv).
 template <typename V, class F>
 int with_kernel(bool dinline, F &&f)
 {
     if (dinline)
         return f(dev::dtans_kernel<V, false, true, true>, dev::dtans_kernel<V, false, false, true>,
-                 dev::dtans_kernel<V, true, false, true>);
+                 dev::dtans_kernel<V, true, false, true>, dev::dtans_kernel<V, false, false, true, true>);
     return f(dev::dtans_kernel<V, false, true, false>, dev::dtans_kernel<V, false, false, false>,
-             dev::dtans_kernel<V, true, false, false>);
+             dev::dtans_kernel<V, true, false, false>, dev::dtans_kernel<V, false, false, false, true>);
 }
 
 template <typename V, class F>
@@ -322,7 +322,8 @@ int configure(dtans_dev *h, const TableBlock &tb, const SmemPlan &sp)
     h->smem = sp.total;
     h->ctas = (int)std::max<int64_t>(1, std::min<int64_t>(sms, ((int64_t)h->chunks.size() + dev::kMaxWarps - 1) / dev::kMaxWarps));
     int per_sm = 0;
-    int rc = with_kernel<V>(tb.dinline, [&](auto kspmv, auto kspmv0, auto kdec) -> int {
+    int rc = with_kernel<V>(tb.dinline, [&](auto kspmv, auto kspmv0, auto kdec, auto kscaled) -> int {
+        CK(cudaFuncSetAttribute(kscaled, cudaFuncAttributeMaxDynamicSharedMemorySize, h->smem), "cudaFuncSetAttribute");
         CK(cudaFuncSetAttribute(kspmv, cudaFuncAttributeMaxDynamicSharedMemorySize, h->smem), "cudaFuncSetAttribute");
         CK(cudaFuncSetAttribute(kspmv0, cudaFuncAttributeMaxDynamicSharedMemorySize, h->smem), "cudaFuncSetAttribute");
         CK(cudaFuncSetAttribute(kdec, cudaFuncAttributeMaxDynamicSharedMemorySize, h->smem), "cudaFuncSetAttribute");
@@ -336,7 +337,9 @@ int configure(dtans_dev *h, const TableBlock &tb, const SmemPlan &sp)
 
 template <typename V>
 int launch(dtans_dev *h, const V *x, const V *y, V *out, const int64_t *row_start, int64_t *cols,
-           void *vals, bool decode_only, cudaStream_t st, int64_t c_lo = -1, int64_t c_hi = -1)
+           void *vals, bool decode_only, cudaStream_t st, int64_t c_lo = -1, int64_t c_hi = -1,
+           const double *sumsq_in = nullptr, double *sumsq_out = nullptr, double *sumsq_zero = nullptr,
+           bool scaled = false)
 {
     if (h->nslices == 0) return DTANS_OK;
     dev::KernelArgs a = h->base;
@@ -353,9 +356,14 @@ int launch(dtans_dev *h, const V *x, const V *y, V *out, const int64_t *row_star
     a.row_start = row_start;
     a.dec_cols = cols;
     a.dec_vals = vals;
+    a.sumsq_in = sumsq_in;
+    a.sumsq_out = sumsq_out;
+    a.sumsq_zero = sumsq_zero;
     if (nch > 0) {
-        with_kernel<V>(h->dinline, [&](auto kspmv, auto kspmv0, auto kdec) -> int {
-            if (decode_only)
+        with_kernel<V>(h->dinline, [&](auto kspmv, auto kspmv0, auto kdec, auto kscaled) -> int {
+            if (scaled)
+                kscaled<<<ctas, h->threads, h->smem, st>>>(a);
+            else if (decode_only)
                 kdec<<<ctas, h->threads, h->smem, st>>>(a);
             else if (y != nullptr)
                 kspmv<<<ctas, h->threads, h->smem, st>>>(a);
@@ -701,6 +709,19 @@ extern "C" int dtans_spmv_f32(dtans_dev *h, const float *x, const float *y, floa
     if (h->precision != 4) return fail(DTANS_E_PARAM, "container precision is f64");
     CK(cudaSetDevice(h->device), "cudaSetDevice");
     return launch<float>(h, x, y, out, nullptr, nullptr, nullptr, false, (cudaStream_t)stream);
+}
+
+extern "C" int dtans_spmv_scaled(dtans_dev *h, const void *x, void *out, const double *sumsq_in, double *sumsq_out,
+                                 double *sumsq_zero, void *stream)
+{
+    if (!h) return fail(DTANS_E_PARAM, "null handle");
+    if (h->base.nlong) return fail(DTANS_E_PARAM, "the scaled SpMV needs a container without long slices");
+    CK(cudaSetDevice(h->device), "cudaSetDevice");
+    if (h->precision == 8)
+        return launch<double>(h, (const double *)x, nullptr, (double *)out, nullptr, nullptr, nullptr, false,
+                              (cudaStream_t)stream, -1, -1, sumsq_in, sumsq_out, sumsq_zero, true);
+    return launch<float>(h, (const float *)x, nullptr, (float *)out, nullptr, nullptr, nullptr, false,
+                         (cudaStream_t)stream, -1, -1, sumsq_in, sumsq_out, sumsq_zero, true);
 }
 
 extern "C" int dtans_check(dtans_dev *h, void *stream)

@@ -122,6 +122,10 @@ struct KernelArgs {
     const LongSlice *longs;
     void *partials;               // V[nparts][32]
     const uint32_t *row_map;      // optional: y/out index of encoded row i (row-reordered P*A)
+    // power iteration (scaled kernel): out = (A x) / sqrt(*sumsq_in), *sumsq_out += sum(out^2)
+    const double *sumsq_in;       // null: no scaling
+    double *sumsq_out;
+    double *sumsq_zero;           // zeroed by the kernel (the accumulator of the next iteration)
     // work distribution over the chunk list
     const ChunkRec *chunks;
     uint32_t chunk_lo, chunk_hi;  // chunks of this launch
@@ -693,10 +697,10 @@ __device__ __forceinline__ void report(const KernelArgs &a, const Ctx &C, bool o
 
 // One slice of a staged chunk: y (or decode positions) from global memory,
 // everything else from shared memory.
-template <typename V, bool kDecode, bool kHasY, bool kDIn>
+template <typename V, bool kDecode, bool kHasY, bool kDIn, bool kScaled>
 __device__ __forceinline__ void decode_slice(const KernelArgs &a, const Ctx &C, const V *__restrict__ x,
                                              SmemSrc src, const uint32_t end, const uint32_t n,
-                                             const uint32_t row, const int lane)
+                                             const uint32_t row, const int lane, const V scale, double &wsum)
 {
     using T = ValueTraits<V>;
     const bool inrow = row < (uint32_t)a.rows;
@@ -713,7 +717,12 @@ __device__ __forceinline__ void decode_slice(const KernelArgs &a, const Ctx &C, 
     const bool ok = decode_range<V, kDecode, kDIn>(a, C, x, src, end, n, maxn, 0u, max_nseg, st, lane);
     report(a, C, ok, st.cur, end, n, st.col, lane);
     if (!kDecode && inrow) {
-        const V res = kHasY ? T::add(st.acc, yv) : st.acc;
+        V res = kHasY ? T::add(st.acc, yv) : st.acc;
+        if (kScaled) {
+            // power iteration: y_k = (A y_{k-1}) / ||y_{k-1}||, sum of y_k^2
+            res = T::mul(res, scale);
+            wsum = __dadd_rn(wsum, __dmul_rn((double)res, (double)res));
+        }
         reinterpret_cast<V *>(a.out)[orow] = res;
     }
 }
@@ -759,7 +768,7 @@ struct WarpCtl {
 // Persistent kernel, one CTA of 32 warps per SM: tables -> shared memory once,
 // then every warp walks chunks (static stride or atomic tickets) through its
 // TMA ring.
-template <typename V, bool kDecode, bool kHasY, bool kDIn>
+template <typename V, bool kDecode, bool kHasY, bool kDIn, bool kScaled = false>
 __global__ void __launch_bounds__(kMaxWarps * 32, 1) dtans_kernel(const KernelArgs a)
 {
     constexpr int kWarps = kMaxWarps;
@@ -781,6 +790,15 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) dtans_kernel(const KernelAr
     }
     const Ctx C = make_ctx<V>(a, lane);
     const V *__restrict__ x = reinterpret_cast<const V *>(a.x);
+    V scale = V(1);
+    double wsum = 0.0;
+    if (kScaled) {
+        if (a.sumsq_in != nullptr) {
+            const double q = *a.sumsq_in;
+            scale = (V)__ddiv_rn(1.0, __dsqrt_rn(q));
+        }
+        if (a.sumsq_zero != nullptr && blockIdx.x == 0 && threadIdx.x == 0) *a.sumsq_zero = 0.0;
+    }
 
     // lane 0's claim pipeline: ticket -> chunk record -> staged buffer
     auto claim = [&]() -> uint32_t {  // lane 0 only; >= chunk_hi: none
@@ -821,8 +839,8 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) dtans_kernel(const KernelAr
             const uint32_t dnext = sh32(buf + 4u * (i + 1u));
             const uint32_t n = sh32(rs + i * 128u);
             const SmemSrc src{st + dcur * 4u};
-            decode_slice<V, kDecode, kHasY, kDIn>(a, C, x, src, dnext - dcur, n,
-                                                   (s0 + i) * kSliceRows + (uint32_t)lane, lane);
+            decode_slice<V, kDecode, kHasY, kDIn, kScaled>(a, C, x, src, dnext - dcur, n,
+                                                            (s0 + i) * kSliceRows + (uint32_t)lane, lane, scale, wsum);
             dcur = dnext;
         }
         __syncwarp();
@@ -838,6 +856,11 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) dtans_kernel(const KernelAr
             b = 0;
             parity ^= 1u;
         }
+    }
+    if (kScaled && a.sumsq_out != nullptr) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) wsum = __dadd_rn(wsum, __shfl_xor_sync(0xFFFFFFFFu, wsum, o));
+        if (lane == 0) atomicAdd(a.sumsq_out, wsum);
     }
 }
 

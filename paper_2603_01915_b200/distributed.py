@@ -96,6 +96,7 @@ class ShardedSpMV:
         self.local = shard(c, int(self.bounds[rank]), int(self.bounds[rank + 1]))
         self.max_rows = max(r1 - r0 for r0, r1 in self.rows_of) if self.rows_of else 0
         self.device = device
+        self._dev = None
         if spmv_fn is None:
             dev = self.local.device(device.index if hasattr(device, "index") and device.index is not None else 0)
             self._dev = dev
@@ -118,8 +119,10 @@ class ShardedSpMV:
         self.local = local
         self.max_rows = max(r1 - r0 for r0, r1 in self.rows_of)
         self.device = device
+        self._dev = None
         if spmv_fn is None:
             dev = local.device(device.index if device is not None and device.index is not None else 0)
+            self._dev = dev
 
             def spmv_fn(x, y, out):
                 return dev.spmv(x, y, out)
@@ -136,17 +139,29 @@ class ShardedSpMV:
         return self.spmv_fn(x, y, out)
 
 
-def power_iteration(op: ShardedSpMV, x0, iters: int, group=None, return_history: bool = False):
+def power_iteration(op: ShardedSpMV, x0, iters: int, group=None, return_history: bool = False,
+                    fused: bool | None = None):
     """x <- A x / ||A x||_2 for ``iters`` iterations over all ranks.
 
     x0: full-length vector on this rank's device (every rank holds the same
     x).  Returns (x, lambda) where lambda = ||A x_{k-1}|| at the last step
-    (the dominant eigenvalue estimate for a Perron matrix)."""
+    (the dominant eigenvalue estimate for a Perron matrix).
+
+    With the CUDA kernel (``fused`` default), one iteration is ONE kernel:
+    the scaled SpMV computes y_k = (A y_{k-1}) / ||y_{k-1}|| and accumulates
+    ||y_k||^2 into a device scalar in its epilogue (dtans_spmv_scaled), so the
+    separate dot / copy / divide passes over y disappear; N>1 adds the NCCL
+    all-reduce of that scalar and the all-gather of y.  x_k = y_{k-1}/||y_{k-1}||
+    is materialised only once, at the end."""
     import torch
     import torch.distributed as dist
     world = op.world
     if len(x0) != op.cols or op.cols != op.global_rows:
         raise ParameterError("power iteration needs a square matrix and a full-length x0")
+    if fused is None:
+        fused = op._dev is not None and op.local.rows > 0 and not return_history
+    if fused:
+        return _power_iteration_fused(op, x0, iters, group)
     x = x0.clone()
     dtype, device = x.dtype, x.device
     pad = torch.zeros(op.max_rows, dtype=dtype, device=device)
@@ -175,6 +190,40 @@ def power_iteration(op: ShardedSpMV, x0, iters: int, group=None, return_history:
             hist.append(float(norm.item()))
     lam = float(lam.item()) if torch.is_tensor(lam) else lam
     return (x, lam, hist) if return_history else (x, lam)
+
+
+def _power_iteration_fused(op: ShardedSpMV, x0, iters: int, group=None):
+    import torch
+    import torch.distributed as dist
+    world = op.world
+    dtype, device = x0.dtype, x0.device
+    # three rotating f64 scalars: step k reads S[k-1] (its scale), adds into
+    # S[k] and zeroes S[k+1]
+    S = torch.zeros(3, dtype=torch.float64, device=device)
+    ybuf = [torch.empty(op.max_rows, dtype=dtype, device=device) for _ in range(2)]
+    if world > 1:
+        gathered = torch.empty(world * op.max_rows, dtype=dtype, device=device)
+        idx = torch.cat([torch.arange(r * op.max_rows, r * op.max_rows + (r1 - r0), device=device)
+                         for r, (r0, r1) in enumerate(op.rows_of)])
+    x = x0
+    rows = op.local.rows
+    k_last = -1
+    for k in range(iters):
+        y = ybuf[k & 1]
+        s_in = S[(k - 1) % 3: (k - 1) % 3 + 1] if k > 0 else None
+        op._dev.spmv_scaled(x, y[:rows], s_in, S[k % 3: k % 3 + 1], S[(k + 1) % 3: (k + 1) % 3 + 1])
+        if world > 1:
+            dist.all_reduce(S[k % 3: k % 3 + 1], group=group)
+            dist.all_gather_into_tensor(gathered, y, group=group)
+            x = torch.index_select(gathered, 0, idx)
+        else:
+            x = y[:rows]
+        k_last = k
+    if k_last < 0:
+        return x0.clone(), float("nan")
+    norm = torch.sqrt(S[k_last % 3])
+    x = (x / norm.to(dtype)).contiguous()
+    return x, float(norm.item())
 
 
 def reference_power_iteration(A_csr, x0: np.ndarray, iters: int):

@@ -49,17 +49,21 @@ def same_bits_or_nan(a, b):
 
 
 LONG_SEG = 64  # slices whose longest row has more segments use the task kernel
+TASK_SEG = 16  # segments per checkpointed task (DTANS_CHUNK default, api.cu)
 
 
 def long_slice_rows(row_start, rows):
-    """Boolean mask of rows that live in long slices (decoded as checkpointed
-    tasks, so their reduction order differs from the reference's)."""
+    """Boolean mask of rows that may be split into several checkpointed
+    tasks (their reduction order differs from the reference's): slices
+    longer than one task (TASK_SEG segments).  Shorter slices are decoded by
+    one warp in lockstep order (main kernel, or a single task) and must match
+    bitwise."""
     nnz_row = np.diff(np.asarray(row_start, dtype=np.int64))
     nseg = (2 * nnz_row + 7) // 8
     ns = -(-rows // 32)
     pad = np.zeros(ns * 32, dtype=np.int64)
     pad[:rows] = nseg
-    long_slice = pad.reshape(ns, 32).max(axis=1) > LONG_SEG
+    long_slice = pad.reshape(ns, 32).max(axis=1) > TASK_SEG
     return np.repeat(long_slice, 32)[:rows]
 
 

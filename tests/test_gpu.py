@@ -155,3 +155,26 @@ def test_row_reordered_rmat(window):
     exp_p = np.empty_like(out)
     exp_p = out[perm.astype(np.int64)]
     assert G.check_spmv(exp_p, ref_p, pm, x, y[perm.astype(np.int64)])
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_power_iteration_fused_matches_unfused(dtype):
+    """dtans_spmv_scaled (scale + sum of squares in the SpMV epilogue) gives
+    the same iterates as the unfused loop (spmv, dot, divide) within the
+    north-star tolerance, and matches numpy."""
+    from paper_2603_01915_b200 import distributed as D
+    m = synth.banded(30000, 32, positive=True, seed=7)
+    if dtype == np.float32:
+        m = P.CsrMatrix(m.rows, m.cols, m.row_start, m.col_idx, m.values.astype(np.float32))
+    c = P.encode_matrix(m)
+    op = D.ShardedSpMV(c, 0, 1, device=torch.device("cuda", 0))
+    tdt = torch.float64 if dtype == np.float64 else torch.float32
+    x0 = torch.full((m.cols,), 1.0 / np.sqrt(m.cols), dtype=tdt, device="cuda")
+    xf, lf = D.power_iteration(op, x0, 25, fused=True)
+    xu, lu = D.power_iteration(op, x0, 25, fused=False)
+    op._dev.check()
+    tol = 1e-12 if dtype == np.float64 else 1e-5
+    assert abs(lf - lu) <= tol * lu
+    assert np.allclose(xf.cpu().numpy(), xu.cpu().numpy(), rtol=10 * tol, atol=10 * tol / np.sqrt(m.cols))
+    xr, lr = D.reference_power_iteration(m, np.full(m.cols, 1.0 / np.sqrt(m.cols)), 25)
+    assert abs(lf - lr) <= 10 * tol * lr
