@@ -198,7 +198,7 @@ SmemPlan plan_smem(const TableBlock &tb, int max_optin, int nring)
     p.off_bars = 0;
     p.off_meta = dev::kMaxWarps * dev::kMaxRing * 8;
     p.off_ctl = 2 * dev::kMaxWarps * dev::kMaxRing * 8;
-    size_t low = (size_t)p.off_ctl + dev::kMaxWarps * 32;
+    size_t low = (size_t)p.off_ctl + dev::kMaxWarps * sizeof(dev::WarpCtl);
     const size_t low0 = low;
     size_t high = (size_t)kTabOff + dev::kTabBytes;
     auto place = [&](size_t bytes) -> int32_t {

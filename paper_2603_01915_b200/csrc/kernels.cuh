@@ -731,6 +731,16 @@ __device__ __forceinline__ void st_shared_v2(uint32_t addr, uint32_t x, uint32_t
 {
     asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(addr), "r"(x), "r"(y) : "memory");
 }
+__device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t x, uint32_t y, uint32_t z, uint32_t w)
+{
+    asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(x), "r"(y), "r"(z), "r"(w) : "memory");
+}
+__device__ __forceinline__ uint4 ld_shared_v4(uint32_t addr)
+{
+    uint4 v;
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr) : "memory");
+    return v;
+}
 __device__ __forceinline__ uint2 ld_shared_v2(uint32_t addr)
 {
     uint2 v;
@@ -763,6 +773,7 @@ __device__ __forceinline__ void stage_chunk(const KernelArgs &a, const bool vali
 struct WarpCtl {
     ChunkRec pend;
     uint32_t pend_c, next_static, pend_ok, pad;
+    uint32_t hdr, rs, st, s0;  // the chunk being decoded (shared addresses), re-read per slice
 };
 
 // Persistent kernel, one CTA of 32 warps per SM: tables -> shared memory once,
@@ -829,20 +840,28 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) dtans_kernel(const KernelAr
         const uint2 md = ld_shared_v2(metas + 8u * b);
         const uint32_t s0 = md.x, k = md.y;
         if (k == 0) break;  // uniform: this warp's chunks are exhausted
-        const uint32_t buf =
-            sb + (uint32_t)a.off_bufs + ((uint32_t)warp * (uint32_t)a.nring + b) * (uint32_t)a.bufb;
-        const uint32_t hw = chunk_hdr_words(k);
-        const uint32_t rs = buf + hw * 4u + (uint32_t)lane * 4u;
-        const uint32_t st = buf + (hw + k * 32u) * 4u;
+        // the chunk's addresses live in the warp's control block and are
+        // re-read per slice (one LDS.128) instead of occupying registers
+        // across the decode
+        const uint32_t ctl_cs = sb + (uint32_t)a.off_ctl + (uint32_t)warp * (uint32_t)sizeof(WarpCtl) + 32u;
+        if (lane == 0) {
+            const uint32_t buf =
+                sb + (uint32_t)a.off_bufs + ((uint32_t)warp * (uint32_t)a.nring + b) * (uint32_t)a.bufb;
+            const uint32_t hw = chunk_hdr_words(k);
+            st_shared_v4(ctl_cs, buf, buf + hw * 4u, buf + (hw + k * 32u) * 4u, s0);
+        }
+        __syncwarp();
         uint32_t dcur = 0;
         for (uint32_t i = 0; i < k; i++) {
-            const uint32_t dnext = sh32(buf + 4u * (i + 1u));
-            const uint32_t n = sh32(rs + i * 128u);
-            const SmemSrc src{st + dcur * 4u};
+            const uint4 cs = ld_shared_v4(ctl_cs);
+            const uint32_t dnext = sh32(cs.x + 4u * (i + 1u));
+            const uint32_t n = sh32(cs.y + i * 128u + (uint32_t)lane * 4u);
+            const SmemSrc src{cs.z + dcur * 4u};
             decode_slice<V, kDecode, kHasY, kDIn, kScaled>(a, C, x, src, dnext - dcur, n,
-                                                            (s0 + i) * kSliceRows + (uint32_t)lane, lane, scale, wsum);
+                                                            (cs.w + i) * kSliceRows + (uint32_t)lane, lane, scale, wsum);
             dcur = dnext;
         }
+        const uint32_t buf = ld_shared_v4(ctl_cs).x;
         __syncwarp();
         if (lane == 0) {
             stage_chunk(a, ctl->pend_ok != 0u, ctl->pend, bars + 8u * b, metas + 8u * b, buf);
@@ -892,6 +911,15 @@ __global__ void __launch_bounds__(kTaskWarps * 32, 1024 / (kTaskWarps * 32)) dta
         const uint32_t n = inrow ? __ldg(a.row_symbols + row) : 0u;
         const uint32_t maxn = __reduce_max_sync(0xFFFFFFFFu, n);
         GmemSrc src{a.stream + __ldg(a.directory + tk.slice), pol};
+        {
+            // pull the task's stream words into L1 up front (coalesced line
+            // prefetches) so the loads on the serial per-segment chain hit L1
+            const uint32_t w0 = tk.ck == 0xFFFFFFFFu ? 0u : tk.cur0;
+            const char *b = reinterpret_cast<const char *>(src.p + w0);
+            const char *e = reinterpret_cast<const char *>(src.p + tk.cur1);
+            for (const char *q = b + 128 * lane; q < e; q += 128 * 32)
+                asm volatile("prefetch.global.L1 [%0];" ::"l"(q));
+        }
         LaneState<V> st;
         st.out_pos = 0;
         if (tk.ck == 0xFFFFFFFFu) {
