@@ -2,9 +2,10 @@
 
 Mirrors the hot-path helpers of /root/reference/pkg/src/csrdtans/sparse.py:
 ``CsrMatrix`` (:54-106), ``coo_to_csr`` (:133-144), ``format_size_bytes``
-(:185-198), ``matrix_deltas`` (:289-299), ``value_patterns`` (:302-309).
-``.mtx`` ingestion and the graph-entropy experiment are out of scope (SURVEY
-§2 row 4b).
+(:185-198), ``matrix_deltas`` (:289-299), ``value_patterns`` (:302-309), and
+the MatrixMarket reader ``parse_mtx`` (:205-264) that feeds the path with
+SuiteSparse matrices.  The graph-entropy experiment is
+out of scope.
 """
 
 from __future__ import annotations
@@ -14,6 +15,10 @@ from dataclasses import dataclass
 import numpy as np
 
 from .errors import ParameterError
+
+
+class MtxFormatError(ValueError):
+    """Malformed MatrixMarket content or duplicate coordinates (sparse.py:22)."""
 
 
 @dataclass
@@ -103,7 +108,7 @@ def coo_to_csr(m: CooMatrix) -> CsrMatrix:
     c = np.asarray(m.col_idx)[order]
     v = np.asarray(m.values)[order]
     if len(r) > 1 and np.any((np.diff(r) == 0) & (np.diff(c) == 0)):
-        raise ParameterError("duplicate (row, col) entry")
+        raise MtxFormatError("duplicate (row, col) entry")
     row_start = np.zeros(m.rows + 1, dtype=np.int64)
     np.cumsum(np.bincount(r, minlength=m.rows), out=row_start[1:])
     return CsrMatrix(m.rows, m.cols, row_start, c.astype(np.int64), v)
@@ -215,3 +220,65 @@ def sort_rows_by_length(m: CsrMatrix, window: int | None = None):
         np.arange(int(row_start[-1]), dtype=np.int64) - np.repeat(row_start[:-1], new_len))
     pm = CsrMatrix(m.rows, m.cols, row_start, np.asarray(m.col_idx)[src], np.asarray(m.values)[src])
     return pm, perm.astype(np.uint32)
+
+
+def parse_mtx(text: str) -> CooMatrix:
+    """Parse MatrixMarket coordinate content (sparse.py:205-264): real /
+    integer / pattern fields, general / symmetric symmetry; symmetric
+    off-diagonal entries are mirrored, pattern entries get value 1.0.
+    Raises MtxFormatError on the same conditions as the reference, checked
+    in the same order."""
+    lines = text.splitlines()
+    if not lines or not lines[0].startswith("%%MatrixMarket"):
+        raise MtxFormatError("missing %%MatrixMarket banner")
+    banner = [tok.lower() for tok in lines[0].split()]
+    if len(banner) != 5:
+        raise MtxFormatError(f"malformed banner: {lines[0]!r}")
+    obj, layout, field, symmetry = banner[1:]
+    if obj != "matrix":
+        raise MtxFormatError(f"unsupported object {obj!r}")
+    if layout != "coordinate":
+        raise MtxFormatError(f"unsupported layout {layout!r} (coordinate only)")
+    if field not in ("real", "integer", "pattern"):
+        raise MtxFormatError(f"unsupported field {field!r}")
+    if symmetry not in ("general", "symmetric"):
+        raise MtxFormatError(f"unsupported symmetry {symmetry!r}")
+    body = [ln for ln in lines[1:] if ln.strip() and not ln.lstrip().startswith("%")]
+    if not body:
+        raise MtxFormatError("missing size line")
+    head = body[0].split()
+    if len(head) != 3:
+        raise MtxFormatError(f"malformed size line: {body[0]!r}")
+    try:
+        rows, cols, nnz = (int(t) for t in head)
+    except ValueError as e:
+        raise MtxFormatError(f"malformed size line: {body[0]!r}") from e
+    if min(rows, cols, nnz) < 0:
+        raise MtxFormatError("negative dimensions")
+    if len(body) - 1 != nnz:
+        raise MtxFormatError(f"expected {nnz} entries, found {len(body) - 1}")
+    width = 2 if field == "pattern" else 3
+    toks = " ".join(body[1:]).split()
+    if len(toks) != nnz * width:
+        raise MtxFormatError("entry lines have the wrong number of fields")
+    try:
+        a = np.asarray(toks, dtype=np.float64).reshape(nnz, width)
+    except ValueError as e:
+        raise MtxFormatError("non-numeric entry") from e
+    r = a[:, 0].astype(np.int64) - 1
+    c = a[:, 1].astype(np.int64) - 1
+    if np.any(a[:, 0] != r + 1) or np.any(a[:, 1] != c + 1):
+        raise MtxFormatError("non-integer index")
+    v = a[:, 2] if width == 3 else np.ones(nnz, dtype=np.float64)
+    if nnz and (r.min() < 0 or r.max() >= rows or c.min() < 0 or c.max() >= cols):
+        raise MtxFormatError("index out of range")
+    if symmetry == "symmetric":
+        off = r != c
+        r, c, v = np.concatenate([r, c[off]]), np.concatenate([c, r[off]]), np.concatenate([v, v[off]])
+    return CooMatrix(rows, cols, r, c, v)
+
+
+def read_mtx(path) -> CsrMatrix:
+    """A MatrixMarket file (e.g. from SuiteSparse) as a CsrMatrix."""
+    with open(path, "r") as f:
+        return coo_to_csr(parse_mtx(f.read()))

@@ -1,0 +1,102 @@
+"""MatrixMarket ingestion (reference sparse.py:205-264; the reference's own
+test cases, tests/test_sparse.py:25-100, restated), plus a cross-check
+against the reference parser when /root/reference is importable here."""
+
+import os
+import sys
+
+import numpy as np
+import pytest
+
+import paper_2603_01915_b200 as P
+from paper_2603_01915_b200 import MtxFormatError, coo_to_csr, parse_mtx
+
+FIG_MTX = """%%MatrixMarket matrix coordinate real general
+4 4 6
+1 2 7.0
+1 4 5.0
+2 1 3.0
+2 3 2.0
+3 2 4.0
+4 4 1.0
+"""
+
+
+def test_running_example_csr():
+    m = coo_to_csr(parse_mtx(FIG_MTX))
+    assert m.values.tolist() == [7, 5, 3, 2, 4, 1]
+    assert m.col_idx.tolist() == [1, 3, 0, 2, 1, 3]
+    assert m.row_start.tolist() == [0, 2, 4, 5, 6]
+
+
+def test_symmetric_mirrors_off_diagonal():
+    coo = parse_mtx("%%MatrixMarket matrix coordinate real symmetric\n2 2 2\n1 1 2.0\n2 1 3.0\n")
+    assert set(zip(coo.row_idx.tolist(), coo.col_idx.tolist(), coo.values.tolist())) == {
+        (0, 0, 2.0), (1, 0, 3.0), (0, 1, 3.0)}
+
+
+def test_pattern_and_integer_fields():
+    coo = parse_mtx("%%MatrixMarket matrix coordinate pattern general\n3 3 1\n3 1\n")
+    assert (coo.row_idx[0], coo.col_idx[0], coo.values[0]) == (2, 0, 1.0)
+    assert parse_mtx("%%MatrixMarket matrix coordinate integer general\n1 1 1\n1 1 7\n").values[0] == 7.0
+
+
+def test_comments_and_blank_lines_skipped():
+    text = "%%MatrixMarket matrix coordinate real general\n% a comment\n\n2 2 1\n% another\n2 2 9.0\n"
+    assert parse_mtx(text).nnz == 1
+
+
+@pytest.mark.parametrize("text", [
+    "no banner\n1 1 0\n",
+    "%%MatrixMarket matrix array real general\n1 1\n1.0\n",
+    "%%MatrixMarket matrix coordinate complex general\n1 1 1\n1 1 1 0\n",
+    "%%MatrixMarket matrix coordinate real skew-symmetric\n1 1 0\n",
+    "%%MatrixMarket matrix coordinate real general\n1 1 1\n2 1 1.0\n",
+    "%%MatrixMarket matrix coordinate real general\n1 1 2\n1 1 1.0\n",
+    "%%MatrixMarket matrix coordinate real general\n1 1 1\n1 1\n",
+    "%%MatrixMarket matrix coordinate real general\n1 1 1\n1.5 1 1.0\n",
+    "%%MatrixMarket matrix coordinate real general\n2 2 1\n1 1 x\n",
+])
+def test_rejects_malformed(text):
+    with pytest.raises(MtxFormatError):
+        parse_mtx(text)
+
+
+def test_duplicates_rejected_as_mtx_error():
+    with pytest.raises(MtxFormatError):
+        coo_to_csr(parse_mtx("%%MatrixMarket matrix coordinate real general\n2 2 2\n1 1 1.0\n1 1 2.0\n"))
+
+
+def test_read_mtx_roundtrip_through_encoder(tmp_path):
+    p = tmp_path / "fig.mtx"
+    p.write_text(FIG_MTX)
+    m = P.read_mtx(str(p))
+    c = P.encode_matrix(m)
+    assert P.size_bytes(c) > 0 and c.nnz == 6
+
+
+REF = "/root/reference/pkg/src"
+
+
+@pytest.mark.skipif(not os.path.isdir(REF), reason="reference not present (GPU box)")
+def test_matches_reference_parser():
+    sys.path.insert(0, REF)
+    try:
+        import csrdtans as R
+    finally:
+        sys.path.remove(REF)
+    rng = np.random.default_rng(3)
+    for sym in ("general", "symmetric"):
+        n, k = 50, 200
+        r = rng.integers(1, n + 1, k)
+        c = rng.integers(1, n + 1, k)
+        if sym == "symmetric":
+            r, c = np.maximum(r, c), np.minimum(r, c)
+        key = np.unique(r * 1000 + c)
+        r, c = key // 1000, key % 1000
+        lines = [f"%%MatrixMarket matrix coordinate real {sym}", f"{n} {n} {len(r)}"]
+        lines += [f"{a} {b} {rng.standard_normal():.17g}" for a, b in zip(r, c)]
+        text = "\n".join(lines) + "\n"
+        a, b = parse_mtx(text), R.parse_mtx(text)
+        for f in ("row_idx", "col_idx", "values"):
+            assert np.array_equal(getattr(a, f), getattr(b, f))
