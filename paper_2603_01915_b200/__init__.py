@@ -14,7 +14,7 @@ from .sparse import (CooMatrix, CsrMatrix, MtxFormatError, coo_to_csr, format_si
                      parse_mtx, read_mtx, reference_spmv, sort_rows_by_length, value_patterns)
 from .tables import ESCAPE, CodingTables, quantize_counts
 from .container import (SLICE_HEIGHT, CsrDtansContainer, DeviceContainer, compression_ratio,
-                        decode_matrix, deserialize, encode_matrix, serialize, size_bytes, spmv)
+                        decode_matrix, deserialize, encode_matrix, load, save, serialize, size_bytes, spmv)
 
 __version__ = "0.1.0"
 
@@ -25,5 +25,5 @@ __all__ = [
     "format_size_bytes", "matrix_deltas", "reference_spmv", "sort_rows_by_length", "value_patterns", "ESCAPE",
     "CodingTables", "quantize_counts", "SLICE_HEIGHT", "CsrDtansContainer", "DeviceContainer",
     "compression_ratio", "decode_matrix", "deserialize", "encode_matrix", "serialize",
-    "size_bytes", "spmv",
+    "size_bytes", "spmv", "load", "save",
 ]

@@ -409,6 +409,10 @@ def serialize(c: CsrDtansContainer) -> bytes:
 
 
 def deserialize(data: bytes) -> CsrDtansContainer:
+    """Parse CDTA v1 bytes (container.py:666-720).  Accepts any buffer
+    (bytes, bytearray, memoryview, mmap); the arrays are zero-copy views of
+    it, so a memory-mapped file is never copied on the host."""
+    data = memoryview(data).cast("B")
     if len(data) < _HEADER.size + _PARAMS.size + 4:
         raise ContainerError("container truncated")
     body, crc_bytes = data[:-4], data[-4:]
@@ -455,8 +459,40 @@ def deserialize(data: bytes) -> CsrDtansContainer:
     return CsrDtansContainer(
         rows=rows, cols=cols, nnz=nnz, precision=precision, params=params,
         permutation_seed=seed, delta_tables=dt, value_tables=vt,
-        row_symbols=row_symbols.astype(np.uint32), directory=directory.astype(np.uint64),
-        stream=stream.astype(np.uint32), table_records=rec)
+        row_symbols=row_symbols.astype(np.uint32, copy=False), directory=directory.astype(np.uint64, copy=False),
+        stream=stream.astype(np.uint32, copy=False), table_records=rec)
+
+
+def save(c: CsrDtansContainer, path) -> int:
+    """Write the CDTA v1 bytes of ``c`` to ``path`` (streamed, running CRC;
+    byte-identical to ``serialize``).  Returns the number of bytes."""
+    p = c.params
+    parts = [
+        _HEADER.pack(MAGIC, FORMAT_VERSION, c.precision, 0, c.rows, c.cols, c.nnz),
+        _PARAMS.pack(p.w_log2, p.k_log2, p.m_log2, p.l, p.o, p.f, c.permutation_seed),
+        memoryview(np.ascontiguousarray(_records(c))).cast("B"),
+        memoryview(np.ascontiguousarray(c.row_symbols, dtype="<u4")).cast("B"),
+        memoryview(np.ascontiguousarray(c.directory, dtype="<u8")).cast("B"),
+        struct.pack("<Q", len(c.stream)),
+        memoryview(np.ascontiguousarray(c.stream, dtype="<u4")).cast("B"),
+    ]
+    crc, n = 0, 0
+    with open(path, "wb") as f:
+        for part in parts:
+            crc = zlib.crc32(part, crc)
+            f.write(part)
+            n += len(part)
+        f.write(struct.pack("<I", crc & 0xFFFFFFFF))
+    return n + 4
+
+
+def load(path) -> CsrDtansContainer:
+    """Memory-map a CDTA file and parse it without copying (the arrays view
+    the mapping); upload with ``.device()`` streams it to HBM."""
+    import mmap
+    with open(path, "rb") as f:
+        mm = mmap.mmap(f.fileno(), 0, access=mmap.ACCESS_READ)
+    return deserialize(mm)
 
 
 def size_bytes(c: CsrDtansContainer) -> int:

@@ -100,3 +100,17 @@ def test_matches_reference_parser():
         a, b = parse_mtx(text), R.parse_mtx(text)
         for f in ("row_idx", "col_idx", "values"):
             assert np.array_equal(getattr(a, f), getattr(b, f))
+
+
+def test_save_load_mmap_roundtrip(tmp_path):
+    """save() streams byte-identical CDTA bytes; load() memory-maps them."""
+    from paper_2603_01915_b200 import synth
+    m = synth.laplacian_2d(120)
+    c = P.encode_matrix(m)
+    path = tmp_path / "lap.cdta"
+    n = P.save(c, str(path))
+    data = path.read_bytes()
+    assert n == len(data) and data == P.serialize(c)
+    c2 = P.load(str(path))
+    assert c2 == c
+    assert not c2.stream.flags.owndata  # a view of the mapping, not a copy
