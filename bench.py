@@ -285,8 +285,9 @@ def main():
     ap.add_argument("--scale", type=float, default=1.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-cusparse", action="store_true")
-    ap.add_argument("--reorder", action="store_true",
-                    help="encode the rows sorted by length (skew toolkit); results in original order")
+    ap.add_argument("--reorder", nargs="?", const="rows", default=None, choices=["rows", "sym"],
+                    help="skew toolkit: 'rows' (default) encodes the rows sorted by length; 'sym' sorts rows "
+                         "and columns by degree; results in the original order")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
 
@@ -316,7 +317,17 @@ def main():
     m, cfg = build_matrix(args.config, args.scale, world, rank)
     t_gen = time.time() - t0
     t0 = time.time()
-    if args.reorder:
+    if args.reorder == "sym":
+        # symmetric degree ordering (sort_symmetric_by_degree): encodes
+        # P*A*P^T; each SpMV gathers x' = x[perm] on the device (timed) and
+        # writes y' in the original row order
+        pm, perm = P.sort_symmetric_by_degree(m)
+        c = P.encode_matrix(pm)
+        c.row_map = perm
+        c.col_map = perm
+        del pm
+        cfg["row_order"] = "rows and columns sorted by degree (P*A*P^T, row_map + col_map, x gather timed)"
+    elif args.reorder:
         # optional row reordering for skewed matrices (sort_rows_by_length):
         # encodes P*A, the kernel writes y' back in the original row order
         pm, perm = P.sort_rows_by_length(m)

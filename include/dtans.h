@@ -161,6 +161,13 @@ int dtans_check(dtans_dev *h, void *stream);
  * encoding of P*A. */
 int dtans_set_row_map(dtans_dev *h, const uint32_t *host_map);
 
+/* Optional column map for a symmetrically reordered container (P*A*P^T from
+ * sort_symmetric_by_degree): every SpMV first gathers x'[j] = x[host_map[j]]
+ * on the device (one coalesced pass over x) and multiplies with x'.  Combine
+ * with dtans_set_row_map(h, same map) for y = A x in the original order.
+ * host_map must be a permutation of [0, cols); NULL clears it. */
+int dtans_set_col_map(dtans_dev *h, const uint32_t *host_map);
+
 /* Number of dtANS kernels launched by this handle so far (bench evidence). */
 int64_t dtans_launch_count(const dtans_dev *h);
 

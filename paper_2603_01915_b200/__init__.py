@@ -11,7 +11,8 @@ C++ encoder and ``spmv`` / ``decode_matrix`` run hand-written CUDA kernels
 from .errors import CodingError, ContainerError, CorruptStream, NativeUnavailable, ParameterError
 from .params import DtansParams, validate_params
 from .sparse import (CooMatrix, CsrMatrix, MtxFormatError, coo_to_csr, format_size_bytes, matrix_deltas,
-                     parse_mtx, read_mtx, reference_spmv, sort_rows_by_length, value_patterns)
+                     parse_mtx, read_mtx, reference_spmv, sort_rows_by_length, sort_symmetric_by_degree,
+                     value_patterns)
 from .tables import ESCAPE, CodingTables, quantize_counts
 from .container import (SLICE_HEIGHT, CsrDtansContainer, DeviceContainer, compression_ratio,
                         decode_matrix, deserialize, encode_matrix, load, save, serialize, size_bytes, spmv)
@@ -21,7 +22,7 @@ __version__ = "0.1.0"
 __all__ = [
     "CodingError", "ContainerError", "CorruptStream", "NativeUnavailable", "ParameterError",
     "DtansParams", "validate_params", "CooMatrix", "CsrMatrix", "MtxFormatError", "coo_to_csr",
-    "parse_mtx", "read_mtx",
+    "parse_mtx", "read_mtx", "sort_symmetric_by_degree",
     "format_size_bytes", "matrix_deltas", "reference_spmv", "sort_rows_by_length", "value_patterns", "ESCAPE",
     "CodingTables", "quantize_counts", "SLICE_HEIGHT", "CsrDtansContainer", "DeviceContainer",
     "compression_ratio", "decode_matrix", "deserialize", "encode_matrix", "serialize",

@@ -24,7 +24,7 @@ EXPORTS = (
     "dtans_last_error", "dtans_abi_version", "dtans_encode", "dtans_encoded_free",
     "dtans_quantize", "dtans_upload", "dtans_free", "dtans_info", "dtans_spmv_f64",
     "dtans_spmv_f32", "dtans_spmv_host", "dtans_decode", "dtans_check",
-    "dtans_launch_count", "dtans_set_row_map", "dtans_spmv_scaled",
+    "dtans_launch_count", "dtans_set_row_map", "dtans_spmv_scaled", "dtans_set_col_map",
 )
 
 
@@ -94,6 +94,7 @@ def lib() -> ctypes.CDLL:
     L.dtans_decode.argtypes = [vp, vp, vp, vp, vp]
     L.dtans_check.argtypes = [vp, vp]
     L.dtans_set_row_map.argtypes = [vp, vp]
+    L.dtans_set_col_map.argtypes = [vp, vp]
     L.dtans_launch_count.argtypes = [vp]
     L.dtans_launch_count.restype = i64
     _lib = L

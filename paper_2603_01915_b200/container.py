@@ -103,6 +103,9 @@ class CsrDtansContainer:
     # row_map[i] is the original row of encoded row i (sort_rows_by_length);
     # spmv then reads y / writes y' in the original order
     row_map: np.ndarray = field(default=None, repr=False)
+    # optional extension (sort_symmetric_by_degree): this container encodes
+    # P*A*P^T; the SpMV gathers x'[j] = x[col_map[j]] on the device first
+    col_map: np.ndarray = field(default=None, repr=False)
     _cache: dict = field(default_factory=dict, repr=False)
 
     @property
@@ -244,6 +247,11 @@ class DeviceContainer:
             if len(rm) != c.rows:
                 raise ParameterError("row_map must have one entry per row")
             _native.check(L.dtans_set_row_map(h, rm.ctypes.data))
+        if c.col_map is not None:
+            cm = np.ascontiguousarray(c.col_map, dtype=np.uint32)
+            if len(cm) != c.cols:
+                raise ParameterError("col_map must have one entry per column")
+            _native.check(L.dtans_set_col_map(h, cm.ctypes.data))
         self.device = int(device)
         self.rows, self.cols, self.nnz, self.precision = c.rows, c.cols, c.nnz, c.precision
         self.row_symbols = c.row_symbols

@@ -43,6 +43,8 @@ struct dtans_dev {
     size_t long_bytes = 0;
     int task_ctas = 0, task_smem = 0, solo_ctas = 0, solo_smem = 0;
     uint32_t *d_row_map = nullptr;  // optional output row map (reordered P*A)
+    uint32_t *d_col_map = nullptr;  // optional column map (symmetric P*A*P^T): x'[j] = x[map[j]]
+    void *d_xperm = nullptr;        // x' scratch (cols values)
     std::vector<dev::ChunkRec> chunks;  // work list of the main kernel (host copy)
     dev::ChunkRec *d_chunks = nullptr;
     bool dinline = false;           // delta symbols inline in the slot table
@@ -335,6 +337,15 @@ int configure(dtans_dev *h, const TableBlock &tb, const SmemPlan &sp)
     return DTANS_OK;
 }
 
+// x'[j] = x[map[j]] (symmetric reordering): one coalesced pass over x'
+template <typename V>
+__global__ void __launch_bounds__(256) permute_x_kernel(const V *__restrict__ x, const uint32_t *__restrict__ map,
+                                                        V *__restrict__ xp, int64_t n)
+{
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x)
+        xp[j] = __ldg(x + __ldg(map + j));
+}
+
 template <typename V>
 int launch(dtans_dev *h, const V *x, const V *y, V *out, const int64_t *row_start, int64_t *cols,
            void *vals, bool decode_only, cudaStream_t st, int64_t c_lo = -1, int64_t c_hi = -1,
@@ -350,6 +361,14 @@ int launch(dtans_dev *h, const V *x, const V *y, V *out, const int64_t *row_star
     const int64_t nch = (int64_t)a.chunk_hi - (int64_t)a.chunk_lo;
     const int ctas = (int)std::max<int64_t>(1, std::min<int64_t>(h->sms, (nch + dev::kMaxWarps - 1) / dev::kMaxWarps));
     if (a.dynamic) CK(cudaMemsetAsync(a.work_counter, 0, sizeof(uint32_t), st), "reset work counter");
+    if (h->d_col_map && !decode_only) {
+        if (c_lo <= 0) {  // once per product (the pipelined host path gathers before its first chunk)
+            const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)h->sms * 8, (h->cols + 255) / 256));
+            permute_x_kernel<V><<<blocks, 256, 0, st>>>(x, h->d_col_map, (V *)h->d_xperm, h->cols);
+            h->launches++;
+        }
+        x = (const V *)h->d_xperm;
+    }
     a.x = x;
     a.y = y;
     a.out = out;
@@ -446,7 +465,7 @@ extern "C" int dtans_upload(const dtans_container_view *c, int device, dtans_dev
     // staging ring: 2 buffers per warp (measured: larger chunks beat a
     // deeper ring; 32 warps x 2 chunks in flight cover the HBM latency)
     const char *er = getenv("DTANS_RING");
-    SmemPlan sp = plan_smem(tb, max_optin, er ? std::max(2, std::min(3, atoi(er))) : 2);
+    SmemPlan sp = plan_smem(tb, max_optin, er ? std::max(1, std::min(3, atoi(er))) : 2);
     if (sp.bufb < 512) {
         delete h;
         return fail(DTANS_E_CUDA, "coding tables leave no shared memory for staging");
@@ -647,6 +666,8 @@ extern "C" void dtans_free(dtans_dev *h)
     if (h->d_base) cudaFree(h->d_base);
     if (h->d_long) cudaFree(h->d_long);
     if (h->d_row_map) cudaFree(h->d_row_map);
+    if (h->d_col_map) cudaFree(h->d_col_map);
+    if (h->d_xperm) cudaFree(h->d_xperm);
     if (h->d_io) cudaFree(h->d_io);
     for (int k = 0; k < kHostChunks; k++) {
         if (h->ev_in[k]) cudaEventDestroy(h->ev_in[k]);
@@ -675,6 +696,8 @@ extern "C" int dtans_set_row_map(dtans_dev *h, const uint32_t *host_map)
     CK(cudaSetDevice(h->device), "cudaSetDevice");
     if (!host_map) {
         if (h->d_row_map) cudaFree(h->d_row_map);
+    if (h->d_col_map) cudaFree(h->d_col_map);
+    if (h->d_xperm) cudaFree(h->d_xperm);
         h->d_row_map = nullptr;
         h->base.row_map = nullptr;
         return DTANS_OK;
@@ -688,6 +711,31 @@ extern "C" int dtans_set_row_map(dtans_dev *h, const uint32_t *host_map)
     if (!h->d_row_map) CK(cudaMalloc(&h->d_row_map, sizeof(uint32_t) * (size_t)std::max<int64_t>(h->rows, 1)), "cudaMalloc row map");
     CK(cudaMemcpy(h->d_row_map, host_map, sizeof(uint32_t) * (size_t)h->rows, cudaMemcpyHostToDevice), "upload row map");
     h->base.row_map = h->d_row_map;
+    return DTANS_OK;
+}
+
+extern "C" int dtans_set_col_map(dtans_dev *h, const uint32_t *host_map)
+{
+    if (!h) return fail(DTANS_E_PARAM, "null handle");
+    CK(cudaSetDevice(h->device), "cudaSetDevice");
+    if (!host_map) {
+        if (h->d_col_map) cudaFree(h->d_col_map);
+        if (h->d_xperm) cudaFree(h->d_xperm);
+        h->d_col_map = nullptr;
+        h->d_xperm = nullptr;
+        return DTANS_OK;
+    }
+    std::vector<uint8_t> seen((size_t)h->cols, 0);
+    for (int64_t i = 0; i < h->cols; i++) {
+        if (host_map[i] >= (uint64_t)h->cols || seen[host_map[i]])
+            return fail(DTANS_E_PARAM, "col map must be a permutation of [0, cols)");
+        seen[host_map[i]] = 1;
+    }
+    const size_t n = (size_t)std::max<int64_t>(h->cols, 1);
+    if (!h->d_col_map) CK(cudaMalloc(&h->d_col_map, sizeof(uint32_t) * n), "cudaMalloc col map");
+    if (!h->d_xperm) CK(cudaMalloc(&h->d_xperm, (size_t)h->precision * n), "cudaMalloc x scratch");
+    CK(cudaMemcpy(h->d_col_map, host_map, sizeof(uint32_t) * (size_t)h->cols, cudaMemcpyHostToDevice),
+       "upload col map");
     return DTANS_OK;
 }
 

@@ -282,3 +282,27 @@ def read_mtx(path) -> CsrMatrix:
     """A MatrixMarket file (e.g. from SuiteSparse) as a CsrMatrix."""
     with open(path, "r") as f:
         return coo_to_csr(parse_mtx(f.read()))
+
+
+def sort_symmetric_by_degree(m: CsrMatrix):
+    """Symmetric degree ordering of a square matrix (skew toolkit, SURVEY
+    §8f item 1): B = P A P^T with rows AND columns in stably descending
+    row-length order.  Rows of similar length share slices (as in
+    sort_rows_by_length), and in power-law graphs the popular columns move
+    to small indices: column deltas shrink (fewer escapes, fewer bytes)
+    and the x gathers concentrate on a hot prefix of x.
+
+    Returns ``(B, perm)`` with ``perm[i]`` = original index of row/column i.
+    Encode B and set ``container.row_map = perm`` and
+    ``container.col_map = perm``: the SpMV then gathers x' = x[perm] on the
+    device and reads y / writes y' in the original order."""
+    if m.rows != m.cols:
+        raise ParameterError("symmetric ordering needs a square matrix")
+    pm, perm = sort_rows_by_length(m)
+    inv = np.empty(m.rows, dtype=np.int64)
+    inv[perm.astype(np.int64)] = np.arange(m.rows, dtype=np.int64)
+    newc = inv[np.asarray(pm.col_idx, dtype=np.int64)]
+    nnz_row = np.diff(np.asarray(pm.row_start, dtype=np.int64))
+    rows = np.repeat(np.arange(pm.rows, dtype=np.int64), nnz_row)
+    o = np.lexsort((newc, rows))
+    return CsrMatrix(pm.rows, pm.cols, pm.row_start, newc[o], np.asarray(pm.values)[o]), perm

@@ -178,3 +178,23 @@ def test_power_iteration_fused_matches_unfused(dtype):
     assert np.allclose(xf.cpu().numpy(), xu.cpu().numpy(), rtol=10 * tol, atol=10 * tol / np.sqrt(m.cols))
     xr, lr = D.reference_power_iteration(m, np.full(m.cols, 1.0 / np.sqrt(m.cols)), 25)
     assert abs(lf - lr) <= 10 * tol * lr
+
+
+def test_symmetric_reordered_rmat():
+    """sort_symmetric_by_degree + row_map + col_map: y = A x in the original
+    order (the device gathers x' = x[perm] first)."""
+    m = synth.rmat(14, 150000, seed=12)
+    x, y = synth.vectors(m)
+    pm, perm = P.sort_symmetric_by_degree(m)
+    c = P.encode_matrix(pm)
+    c.row_map = perm
+    c.col_map = perm
+    out = P.spmv(c, x, y)
+    p64 = perm.astype(np.int64)
+    ref_p = O.spmv(O.parse(P.serialize(c)), x[p64], y[p64], threads=8)
+    assert G.check_spmv(out[p64], ref_p, pm, x[p64], y[p64])
+    # and through the device-tensor path
+    dev = c.device(0)
+    o2 = dev.spmv(torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda())
+    dev.check()
+    assert G.same_bits_or_nan(o2.cpu().numpy(), out)

@@ -114,3 +114,18 @@ def test_save_load_mmap_roundtrip(tmp_path):
     c2 = P.load(str(path))
     assert c2 == c
     assert not c2.stream.flags.owndata  # a view of the mapping, not a copy
+
+
+def test_sort_symmetric_by_degree_is_pap():
+    from paper_2603_01915_b200 import synth
+    m = synth.rmat(9, 3000, seed=2)
+    b, perm = P.sort_symmetric_by_degree(m)
+    import scipy.sparse as sp
+    A = sp.csr_matrix((m.values, m.col_idx, m.row_start), shape=(m.rows, m.cols))
+    B = sp.csr_matrix((b.values, b.col_idx, b.row_start), shape=(b.rows, b.cols))
+    p = perm.astype(np.int64)
+    assert (A[p][:, p] != B).nnz == 0
+    nnz_row = np.diff(b.row_start)
+    assert np.all(np.diff(nnz_row) <= 0)  # rows by descending length
+    for i in range(b.rows):  # columns ascending within rows
+        assert np.all(np.diff(b.col_idx[b.row_start[i]:b.row_start[i + 1]]) > 0)
