@@ -15,7 +15,7 @@
 
 using namespace dtans;
 
-constexpr int kHostChunks = 8;
+constexpr int kHostChunks = 32;  // max pipeline stages of the host-buffer path
 constexpr size_t kRawStreamPad = dev::kStreamPadWords;
 
 struct dtans_dev {
@@ -809,7 +809,9 @@ extern "C" int dtans_spmv_host(dtans_dev *h, const void *x, const void *y, void 
     // the D2H of a chunk overlaps the H2D and decode of the next.  Containers
     // with long slices or dynamic scheduling use one launch.
     const int64_t nchunks = (int64_t)h->chunks.size();
-    const bool chunked = h->base.nlong == 0 && !h->base.dynamic && nchunks >= 64 * kHostChunks;
+    const char *eh = getenv("DTANS_HOST_STAGES");
+    const int stages = std::max(1, std::min(kHostChunks, eh ? atoi(eh) : 8));
+    const bool chunked = h->base.nlong == 0 && !h->base.dynamic && nchunks >= 64 * stages;
     if (!h->st_in) {
         CK(cudaStreamCreateWithFlags(&h->st_in, cudaStreamNonBlocking), "stream");
         CK(cudaStreamCreateWithFlags(&h->st_comp, cudaStreamNonBlocking), "stream");
@@ -819,7 +821,7 @@ extern "C" int dtans_spmv_host(dtans_dev *h, const void *x, const void *y, void 
             CK(cudaEventCreateWithFlags(&h->ev_done[k], cudaEventDisableTiming), "event");
         }
     }
-    const int nch = chunked ? kHostChunks : 1;
+    const int nch = chunked ? stages : 1;
     CK(cudaMemcpyAsync(dx, x, es * (size_t)h->cols, cudaMemcpyHostToDevice, h->st_in), "H2D x");
     for (int k = 0; k < nch; k++) {
         // chunks [c0, c1) cover rows [r0, r1) (natural order when chunked)
