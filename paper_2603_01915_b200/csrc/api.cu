@@ -454,7 +454,10 @@ extern "C" int dtans_upload(const dtans_container_view *c, int device, dtans_dev
 
     // per-slice cost (segments of the longest row) and the long-slice split
     const char *e1 = getenv("DTANS_LONG_SEG"), *e2 = getenv("DTANS_CHUNK");
-    const int long_seg = e1 ? atoi(e1) : 64, chunk = e2 ? atoi(e2) : 16;
+    // chunked slices have max_nseg <= long_seg <= kMetaMaxNseg (slice_meta field)
+    const int long_seg = std::min<int>(e1 ? atoi(e1) : 64, (int)dev::kMetaMaxNseg);
+    const int chunk = e2 ? atoi(e2) : 16;
+    const bool pads_ok = tb.nd > 0 && tb.nv > 0;
     std::vector<uint32_t> cost((size_t)nsl);
     for (int64_t s = 0; s < nsl; s++) {
         uint32_t m = 0;
@@ -597,7 +600,19 @@ extern "C" int dtans_upload(const dtans_container_view *c, int device, dtans_dev
                     const int64_t s0 = r.s0, k = r.kw & 0xFF;
                     uint32_t *p = blob.data() + r.off;
                     const uint64_t base = c->directory[s0];
-                    for (int64_t i = 0; i <= k; i++) p[i] = (uint32_t)(c->directory[s0 + i] - base);
+                    for (int64_t i = 0; i < k; i++) {
+                        // slice metadata word (kernels.cuh slice_meta)
+                        const int64_t sr0 = (s0 + i) * kSlice;
+                        uint32_t maxn = 0, minseg = 0xFFFFFFFFu;
+                        for (int64_t l = 0; l < kSlice; l++) {
+                            const uint32_t n = sr0 + l < c->rows ? c->row_symbols[sr0 + l] : 0u;
+                            maxn = std::max(maxn, n);
+                            minseg = std::min(minseg, (n + 7u) / 8u);
+                        }
+                        const uint32_t mseg = (maxn + 7u) / 8u;
+                        const uint32_t np = pads_ok && mseg > 0 ? (maxn - 8u * (mseg - 1u)) / 2u : 4u;
+                        p[i] = dev::slice_meta((uint32_t)(c->directory[s0 + i + 1] - base), mseg, minseg, np);
+                    }
                     p += dev::chunk_hdr_words((uint32_t)k);
                     const int64_t r0 = s0 * kSlice, r1 = std::min<int64_t>((s0 + k) * kSlice, c->rows);
                     memcpy(p, c->row_symbols + r0, sizeof(uint32_t) * (size_t)(r1 - r0));

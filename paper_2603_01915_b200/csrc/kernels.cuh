@@ -79,15 +79,28 @@ template <> struct ValueTraits<float> {
 
 // A chunk: slices [s0, s0 + k) (k = kw & 0xFF) stored as one contiguous
 // blob of kw >> 8 words at word offset `off` of the chunk-blob array:
-//   [hdr: k+1 u32 stream offsets, padded to 4][row_symbols: k*32 u32][stream words, padded to 4]
-// hdr[i] = directory[s0+i] - directory[s0] (the reference's word ranges,
-// container.py:296-317, relative to the chunk).
+//   [hdr: k u32 slice words, padded to 4][row_symbols: k*32 u32][stream words, padded to 4]
+// hdr[i] describes slice s0+i (host-computed once at upload, slice_meta()):
+//   bits  0-15  directory[s0+i+1] - directory[s0]: the end of the slice's
+//               words relative to the chunk (container.py:296-317); the
+//               start is the previous slice's end (0 for i = 0)
+//   bits 16-22  max_nseg  = ceil(max row_symbols / 8) over the slice's 32 rows
+//   bits 23-29  min_nseg  (rows past the matrix count as 0)
+//   bits 30-31  np - 1: pairs the final segment decodes (4 if pads may escape)
+// so the per-slice warp reductions and final-segment arithmetic are paid once
+// on the host instead of once per slice per SpMV.
 struct __align__(16) ChunkRec {
     unsigned long long off;
     uint32_t s0;
     uint32_t kw;
 };
-__host__ __device__ constexpr uint32_t chunk_hdr_words(uint32_t k) { return (k + 4u) & ~3u; }
+__host__ __device__ constexpr uint32_t chunk_hdr_words(uint32_t k) { return (k + 3u) & ~3u; }
+constexpr uint32_t kMetaMaxNseg = 127u;  // max_nseg field width (7 bits)
+__host__ __device__ constexpr uint32_t slice_meta(uint32_t end_rel, uint32_t max_nseg, uint32_t min_nseg,
+                                                  uint32_t np)
+{
+    return end_rel | (max_nseg << 16) | (min_nseg << 23) | ((np - 1u) & 3u) << 30;
+}
 
 struct KernelArgs {
     const uint32_t *tables;       // shared-memory image [off_img, off_img + table_bytes) (global copy)
@@ -624,13 +637,10 @@ __device__ __forceinline__ void final_segment(const KernelArgs &a, const Ctx &C,
 template <typename V, bool kDecode, bool kDIn, class Src>
 __device__ __forceinline__ bool decode_range(const KernelArgs &a, const Ctx &C, const V *__restrict__ x,
                                              Src &src, const uint32_t end, const uint32_t n,
-                                             const uint32_t maxn, const uint32_t j0, const uint32_t j1,
-                                             LaneState<V> &st, const int lane)
+                                             const uint32_t max_nseg, const uint32_t min_nseg, const uint32_t np,
+                                             const uint32_t j0, const uint32_t j1, LaneState<V> &st, const int lane)
 {
-    const uint32_t FULL = 0xFFFFFFFFu;
     const uint32_t nseg = (n + 7u) >> 3;
-    const uint32_t max_nseg = (maxn + 7u) >> 3;
-    const uint32_t min_nseg = __reduce_min_sync(FULL, nseg);
     const uint32_t jfull = min(j1, max_nseg - 1u);  // segments that fold digits: [j0, jfull)
     // segments where every lane is active and folds digits, then segments
     // where some lane does (per-lane predicates)
@@ -649,10 +659,9 @@ __device__ __forceinline__ bool decode_range(const KernelArgs &a, const Ctx &C, 
         if (st.cur > end) return false;
     }
     if (j1 == max_nseg && max_nseg > 0) {
-        // pairs the final segment needs: (maxn - 8 jf) / 2 (n is even); all 4
-        // lookups are needed only when pads may escape (escape-only table)
+        // np = pairs the final segment needs (all 4 lookups only when pads
+        // may escape: escape-only table)
         const uint32_t jf = max_nseg - 1;
-        const uint32_t np = C.pads_ok ? (maxn - 8u * jf) >> 1 : 4u;
         src.prepare(st.cur);
         switch (np) {  // uniform
         case 1: final_segment<V, kDecode, kDIn, 1>(a, C, x, src, jf, n, st); break;
@@ -662,6 +671,18 @@ __device__ __forceinline__ bool decode_range(const KernelArgs &a, const Ctx &C, 
         }
     }
     return true;
+}
+
+// The slice shape from the lanes' row lengths (long-slice tasks, which have
+// no host-built slice metadata): max_nseg, min_nseg and the final segment's
+// pair count, as slice_meta() records them for chunked slices.
+__device__ __forceinline__ void slice_shape(const Ctx &C, const uint32_t n, uint32_t &max_nseg, uint32_t &min_nseg,
+                                            uint32_t &np)
+{
+    const uint32_t maxn = __reduce_max_sync(0xFFFFFFFFu, n);
+    max_nseg = (maxn + 7u) >> 3;
+    min_nseg = __reduce_min_sync(0xFFFFFFFFu, (n + 7u) >> 3);
+    np = C.pads_ok && max_nseg > 0 ? (maxn - 8u * (max_nseg - 1u)) >> 1 : 4u;
 }
 
 // init events (container.py:426-429): 3 words per active lane
@@ -699,13 +720,15 @@ __device__ __forceinline__ void report(const KernelArgs &a, const Ctx &C, bool o
 // everything else from shared memory.
 template <typename V, bool kDecode, bool kHasY, bool kDIn, bool kScaled>
 __device__ __forceinline__ void decode_slice(const KernelArgs &a, const Ctx &C, const V *__restrict__ x,
-                                             SmemSrc src, const uint32_t end, const uint32_t n,
-                                             const uint32_t row, const int lane, const V scale, double &wsum)
+                                             SmemSrc src, const uint32_t end, const uint32_t meta,
+                                             const uint32_t n, const uint32_t row, const int lane, const V scale,
+                                             double &wsum)
 {
     using T = ValueTraits<V>;
     const bool inrow = row < (uint32_t)a.rows;
-    const uint32_t maxn = __reduce_max_sync(0xFFFFFFFFu, n);
-    const uint32_t max_nseg = (maxn + 7u) >> 3;
+    const uint32_t max_nseg = (meta >> 16) & 0x7Fu;
+    const uint32_t min_nseg = (meta >> 23) & 0x7Fu;
+    const uint32_t np = (meta >> 30) + 1u;
     uint32_t orow = row;
     if (a.row_map != nullptr && inrow) orow = __ldg(a.row_map + row);
     V yv = V(0);
@@ -714,7 +737,8 @@ __device__ __forceinline__ void decode_slice(const KernelArgs &a, const Ctx &C, 
     st.out_pos = 0;
     if (kDecode && inrow) st.out_pos = __ldg(a.row_start + row);
     init_state<V>(C, src, n, st);
-    const bool ok = decode_range<V, kDecode, kDIn>(a, C, x, src, end, n, maxn, 0u, max_nseg, st, lane);
+    const bool ok =
+        decode_range<V, kDecode, kDIn>(a, C, x, src, end, n, max_nseg, min_nseg, np, 0u, max_nseg, st, lane);
     report(a, C, ok, st.cur, end, n, st.col, lane);
     if (!kDecode && inrow) {
         V res = kHasY ? T::add(st.acc, yv) : st.acc;
@@ -854,10 +878,11 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) dtans_kernel(const KernelAr
         uint32_t dcur = 0;
         for (uint32_t i = 0; i < k; i++) {
             const uint4 cs = ld_shared_v4(ctl_cs);
-            const uint32_t dnext = sh32(cs.x + 4u * (i + 1u));
+            const uint32_t meta = sh32(cs.x + 4u * i);
+            const uint32_t dnext = meta & 0xFFFFu;
             const uint32_t n = sh32(cs.y + i * 128u + (uint32_t)lane * 4u);
             const SmemSrc src{cs.z + dcur * 4u};
-            decode_slice<V, kDecode, kHasY, kDIn, kScaled>(a, C, x, src, dnext - dcur, n,
+            decode_slice<V, kDecode, kHasY, kDIn, kScaled>(a, C, x, src, dnext - dcur, meta, n,
                                                             (cs.w + i) * kSliceRows + (uint32_t)lane, lane, scale, wsum);
             dcur = dnext;
         }
@@ -909,7 +934,8 @@ __global__ void __launch_bounds__(kTaskWarps * 32, 1024 / (kTaskWarps * 32)) dta
         const uint32_t row = tk.slice * kSliceRows + lane;
         const bool inrow = row < (uint32_t)a.rows;
         const uint32_t n = inrow ? __ldg(a.row_symbols + row) : 0u;
-        const uint32_t maxn = __reduce_max_sync(0xFFFFFFFFu, n);
+        uint32_t max_nseg, min_nseg, np;
+        slice_shape(C, n, max_nseg, min_nseg, np);
         GmemSrc src{a.stream + __ldg(a.directory + tk.slice), pol};
         {
             // pull the task's stream words into L1 up front (coalesced line
@@ -939,7 +965,8 @@ __global__ void __launch_bounds__(kTaskWarps * 32, 1024 / (kTaskWarps * 32)) dta
         }
         // decoding: every segment before j0 of an active lane was full (4 pairs)
         if (kDecode && inrow) st.out_pos = __ldg(a.row_start + row) + 4ll * tk.j0;
-        const bool ok = decode_range<V, kDecode, kDIn>(a, C, x, src, tk.cur1, n, maxn, tk.j0, tk.j1, st, lane);
+        const bool ok = decode_range<V, kDecode, kDIn>(a, C, x, src, tk.cur1, n, max_nseg, min_nseg, np, tk.j0,
+                                                       tk.j1, st, lane);
         report(a, C, ok, st.cur, tk.cur1, tk.last ? n : 0u, st.col, lane);
         if (!kDecode) {
             if (tk.last && tk.j0 == 0) {
