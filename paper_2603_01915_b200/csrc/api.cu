@@ -468,7 +468,11 @@ extern "C" int dtans_upload(const dtans_container_view *c, int device, dtans_dev
     // staging ring: 2 buffers per warp (measured: larger chunks beat a
     // deeper ring; 32 warps x 2 chunks in flight cover the HBM latency)
     const char *er = getenv("DTANS_RING");
-    SmemPlan sp = plan_smem(tb, max_optin, er ? std::max(1, std::min(3, atoi(er))) : 2);
+    // DTANS_SMEM_KB caps the main kernel's shared memory (the rest of the
+    // SM's 256 KB L1/shared array becomes L1 cache for the x gathers)
+    const char *ek = getenv("DTANS_SMEM_KB");
+    const int smem_cap = ek ? std::min(max_optin, atoi(ek) * 1024) : max_optin;
+    SmemPlan sp = plan_smem(tb, smem_cap, er ? std::max(1, std::min(3, atoi(er))) : 2);
     if (sp.bufb < 512) {
         delete h;
         return fail(DTANS_E_CUDA, "coding tables leave no shared memory for staging");
