@@ -82,6 +82,17 @@ int dtans_encode(const dtans_csr_view *m, const dtans_encode_opts *opts,
                  dtans_encoded *out);
 void dtans_encoded_free(dtans_encoded *e);
 
+/* The same container bytes as dtans_encode (byte-identical to the reference
+ * encode_matrix, container.py:126-204), with the per-symbol passes on CUDA
+ * device `device`: validation + delta/value extraction (sparse.py:76-91,
+ * 289-309), the distributions (container.py:112-114) by device radix sort +
+ * run-length encode, the base pass and the backward digit pass + warp
+ * interleave (codec.py:278-368, container.py:254-317), one warp per slice.
+ * quantize/build_tables (entropy.py:223-436) run on the host (the one
+ * floating-point step).  Host CSR in, host container out; nnz < 2^31. */
+int dtans_encode_device(const dtans_csr_view *m, const dtans_encode_opts *opts, int device,
+                        dtans_encoded *out);
+
 /* Replaces quantize (entropy.py:223-321) for one domain.  symbols ascending,
  * counts >= 1.  Writes mult[n] (0 = escaped), *esc_mult, *esc_slots.
  * never_retain: n_never symbols that are always escaped. */

@@ -152,10 +152,13 @@ class CsrDtansContainer:
 def encode_matrix(m: CsrMatrix, params: DtansParams | None = None,
                   value_width: int | None = None,
                   permutation_seed: int | None = DEFAULT_PERMUTATION_SEED,
-                  *, threads: int = 0) -> CsrDtansContainer:
+                  *, threads: int = 0, device: int | None = None) -> CsrDtansContainer:
     """Compress ``m``; bytes identical to the reference encoder
     (container.py:126-204).  ``threads`` (keyword-only, new) sets the C++
-    encoder's thread count (0 = all cores)."""
+    encoder's thread count (0 = all cores).  ``device`` (keyword-only, new):
+    run the per-symbol passes on that CUDA device (dtans_encode_device: the
+    distributions, the base pass and the digit pass + warp interleave; the
+    same bytes); None = the host encoder."""
     if len(m.row_start) != m.rows + 1:
         raise ParameterError("row_start must have rows + 1 entries")
     params = params or DtansParams.production()
@@ -186,7 +189,10 @@ def encode_matrix(m: CsrMatrix, params: DtansParams | None = None,
                               perm_d.ctypes.data if perm_d is not None else None,
                               perm_v.ctypes.data if perm_v is not None else None, threads)
     enc = _native.Encoded()
-    _native.check(L.dtans_encode(ctypes.byref(view), ctypes.byref(opts), ctypes.byref(enc)))
+    if device is None:
+        _native.check(L.dtans_encode(ctypes.byref(view), ctypes.byref(opts), ctypes.byref(enc)))
+    else:
+        _native.check(L.dtans_encode_device(ctypes.byref(view), ctypes.byref(opts), int(device), ctypes.byref(enc)))
     try:
         rec_bytes = ctypes.string_at(enc.tables, params.k * enc.rec_size)
         rec = np.frombuffer(rec_bytes, dtype=_SLOT_DTYPE[precision]).copy()

@@ -25,6 +25,7 @@
 #include <vector>
 
 #include "common.h"
+#include "encoder_internal.h"
 
 namespace dtans {
 
@@ -36,11 +37,6 @@ namespace {
 // ----------------------------------------------------------------------------
 // Distributions (container.py:112-114): sorted unique symbols with counts.
 
-struct Dist {
-    std::vector<uint64_t> sym;
-    std::vector<int64_t> cnt;
-    int64_t total = 0;
-};
 
 static void rle_sorted(const uint64_t *a, size_t n, std::vector<uint64_t> &s,
                        std::vector<int64_t> &c)
@@ -282,56 +278,7 @@ class Quantizer {
 // ----------------------------------------------------------------------------
 // Coding tables (entropy.py:333-436) + encoder-side inverse maps.
 
-struct SymMap {  // open addressing, symbol -> retained id
-    std::vector<uint64_t> keys;
-    std::vector<int32_t> vals;
-    uint64_t mask = 0;
-    int shift = 0;
-    void init(size_t n)
-    {
-        size_t cap = 16;
-        while (cap < 4 * n) cap <<= 1;
-        keys.assign(cap, 0);
-        vals.assign(cap, -1);
-        mask = cap - 1;
-        shift = 64 - __builtin_ctzll(cap);
-    }
-    size_t h(uint64_t k) const { return (size_t)((k * 0x9E3779B97F4A7C15ull) >> shift); }
-    void put(uint64_t k, int32_t v)
-    {
-        size_t i = h(k);
-        while (vals[i] >= 0) i = (i + 1) & mask;
-        keys[i] = k;
-        vals[i] = v;
-    }
-    int32_t get(uint64_t k) const
-    {
-        size_t i = h(k);
-        while (vals[i] >= 0) {
-            if (keys[i] == k) return vals[i];
-            i = (i + 1) & mask;
-        }
-        return -1;
-    }
-};
 
-struct Domain {
-    // slot arrays (decode view)
-    std::vector<uint64_t> sym;
-    std::vector<uint8_t> dig;
-    std::vector<uint16_t> base;
-    std::vector<uint8_t> esc;
-    // encoder view
-    int32_t esc_base = 0;            // 0: no escape entry
-    std::vector<uint16_t> esc_slot;  // (ESCAPE, d) -> slot, full-base run only
-    std::vector<uint16_t> id_base;
-    std::vector<uint32_t> id_off;
-    std::vector<uint16_t> slot_by_digit;
-    SymMap map;
-    bool has_pad = false;
-    int32_t pad_id = -1;
-    int payload_words = 1;
-};
 
 static bool build_domain(const Dist &dist, const Quant &q, const uint32_t *perm,
                          int32_t k, int payload_words, Domain &D)
@@ -405,6 +352,7 @@ static bool build_domain(const Dist &dist, const Quant &q, const uint32_t *perm,
         }
     }
     D.has_pad = D.pad_id >= 0;
+    D.ret_sym = ret_sym;
     D.map.init((size_t)nret);
     for (int32_t i = 0; i < nret; i++) D.map.put(ret_sym[i], i);
     D.payload_words = payload_words;
@@ -641,6 +589,50 @@ static void parallel_for(int nthreads, int64_t n, F fn)
 }
 
 }  // namespace
+
+int prepare_tables(const Dist &ddist, const Dist &vdist, int prec, const dtans_encode_opts *opts,
+                   uint8_t *tables, Domain &Dd, Domain &Dv)
+{
+    const int32_t K = 1 << opts->k_log2, M = 1 << opts->m_log2;
+    const uint64_t vsent = prec == 8 ? ~0ull : 0xFFFFFFFFull;
+    auto quant = [&](const Dist &d, uint64_t sentinel, int raw, Quant &q) -> bool {
+        std::vector<char> never(d.sym.size(), 0);
+        auto it = std::lower_bound(d.sym.begin(), d.sym.end(), sentinel);
+        if (it != d.sym.end() && *it == sentinel) never[it - d.sym.begin()] = 1;
+        Quantizer qz(d.cnt, never, K, M, raw);
+        return qz.run(q);
+    };
+    Quant qd, qv;
+    if (!quant(ddist, kDeltaSentinel, 32, qd) || !quant(vdist, vsent, 8 * prec, qv))
+        return fail(DTANS_E_PARAM, "no feasible quantization for these parameters");
+    if (!build_domain(ddist, qd, opts->perm_delta, K, 1, Dd) ||
+        !build_domain(vdist, qv, opts->perm_value, K, prec / 4, Dv))
+        return fail(DTANS_E_PARAM, "permutation must be a bijection on slots");
+
+    // tables block (container.py:612-625)
+    const int rec = prec == 8 ? 16 : 12;
+    for (int32_t j = 0; j < K; j++) {
+        uint8_t *r = tables + (size_t)j * rec;
+        const uint64_t vs = Dv.esc[j] ? vsent : Dv.sym[j];
+        const uint32_t ds = Dd.esc[j] ? (uint32_t)kDeltaSentinel : (uint32_t)Dd.sym[j];
+        if (prec == 8) {
+            memcpy(r, &vs, 8);
+            memcpy(r + 8, &ds, 4);
+            r += 12;
+        } else {
+            const uint32_t v32 = (uint32_t)vs;
+            memcpy(r, &v32, 4);
+            memcpy(r + 4, &ds, 4);
+            r += 8;
+        }
+        r[0] = Dd.dig[j];
+        r[1] = (uint8_t)(Dd.base[j] - 1);
+        r[2] = Dv.dig[j];
+        r[3] = (uint8_t)(Dv.base[j] - 1);
+    }
+    return DTANS_OK;
+}
+
 }  // namespace dtans
 
 using namespace dtans;
@@ -695,7 +687,7 @@ extern "C" int dtans_encode(const dtans_csr_view *m, const dtans_encode_opts *op
         if (opts->k_log2 != kKLog2) return fail(DTANS_E_PARAM, "this build implements k = 4096");
         if (opts->m_log2 < 1 || opts->m_log2 > 8)
             return fail(DTANS_E_PARAM, "slot records store base - 1 in one byte; m <= 256");
-        const int32_t K = 1 << opts->k_log2, M = 1 << opts->m_log2;
+        const int32_t K = 1 << opts->k_log2;
         if (m->rows < 0 || m->cols < 0) return fail(DTANS_E_PARAM, "negative dimensions");
         if (m->cols > (int64_t)1 << 32 || m->rows > (int64_t)1 << 32)
             return fail(DTANS_E_PARAM, "indices must fit 32 bits");
@@ -755,24 +747,7 @@ extern "C" int dtans_encode(const dtans_csr_view *m, const dtans_encode_opts *op
         Dist ddist = merge_runs(dsy, dct);
         Dist vdist = merge_runs(vsy, vct);
 
-        // quantize x2 (container.py:155-158)
-        const uint64_t vsent = prec == 8 ? ~0ull : 0xFFFFFFFFull;
-        auto quant = [&](const Dist &d, uint64_t sentinel, int raw, Quant &q) -> bool {
-            std::vector<char> never(d.sym.size(), 0);
-            auto it = std::lower_bound(d.sym.begin(), d.sym.end(), sentinel);
-            if (it != d.sym.end() && *it == sentinel) never[it - d.sym.begin()] = 1;
-            Quantizer qz(d.cnt, never, K, M, raw);
-            return qz.run(q);
-        };
-        Quant qd, qv;
-        if (!quant(ddist, kDeltaSentinel, 32, qd) || !quant(vdist, vsent, 8 * prec, qv))
-            return fail(DTANS_E_PARAM, "no feasible quantization for these parameters");
         Domain Dd, Dv;
-        if (!build_domain(ddist, qd, opts->perm_delta, K, 1, Dd) ||
-            !build_domain(vdist, qv, opts->perm_value, K, prec / 4, Dv))
-            return fail(DTANS_E_PARAM, "permutation must be a bijection on slots");
-
-        // tables block (container.py:612-625)
         const int rec = prec == 8 ? 16 : 12;
         out->tables = (uint8_t *)malloc((size_t)K * rec);
         out->row_symbols = (uint32_t *)malloc(sizeof(uint32_t) * (size_t)std::max<int64_t>(rows, 1));
@@ -781,24 +756,12 @@ extern "C" int dtans_encode(const dtans_csr_view *m, const dtans_encode_opts *op
             dtans_encoded_free(out);
             return fail(DTANS_E_NOMEM, "host allocation failed");
         }
-        for (int32_t j = 0; j < K; j++) {
-            uint8_t *r = out->tables + (size_t)j * rec;
-            const uint64_t vs = Dv.esc[j] ? vsent : Dv.sym[j];
-            const uint32_t ds = Dd.esc[j] ? (uint32_t)kDeltaSentinel : (uint32_t)Dd.sym[j];
-            if (prec == 8) {
-                memcpy(r, &vs, 8);
-                memcpy(r + 8, &ds, 4);
-                r += 12;
-            } else {
-                const uint32_t v32 = (uint32_t)vs;
-                memcpy(r, &v32, 4);
-                memcpy(r + 4, &ds, 4);
-                r += 8;
+        {
+            const int rc = prepare_tables(ddist, vdist, prec, opts, out->tables, Dd, Dv);
+            if (rc) {
+                dtans_encoded_free(out);
+                return rc;
             }
-            r[0] = Dd.dig[j];
-            r[1] = (uint8_t)(Dd.base[j] - 1);
-            r[2] = Dv.dig[j];
-            r[3] = (uint8_t)(Dv.base[j] - 1);
         }
         for (int64_t i = 0; i < rows; i++) out->row_symbols[i] = (uint32_t)(2 * (rs[i + 1] - rs[i]));
 
