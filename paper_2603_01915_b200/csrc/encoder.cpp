@@ -133,12 +133,28 @@ class Quantizer {
         const int64_t n = (int64_t)counts.size();
         total_ = 0;
         for (int64_t c : counts) total_ += c;
-        std::vector<int64_t> order(n);
-        for (int64_t i = 0; i < n; i++) order[i] = i;
-        // sorted(range(n), key=lambda i: (-counts[i], i))
-        std::stable_sort(order.begin(), order.end(), [&](int64_t a, int64_t b) {
-            return counts[a] > counts[b];
-        });
+        // sorted(range(n), key=lambda i: (-counts[i], i)) minus never_retain:
+        // only the first min(n_eligible, k) entries are ever retained, so
+        // only the first top = k + |never| + 1 of that order are built: the
+        // top-th largest count (selection on a contiguous copy), every index
+        // above it, then the tied ones in index order (the order is total).
+        int64_t n_never = 0;
+        for (int64_t i = 0; i < n; i++) n_never += never[i] ? 1 : 0;
+        n_eligible_ = n - n_never;
+        const int64_t top = std::min<int64_t>(n, (int64_t)k + n_never + 1);
+        std::vector<int64_t> order;
+        order.reserve((size_t)top);
+        if (top > 0) {
+            std::vector<int64_t> cs(counts.begin(), counts.end());
+            std::nth_element(cs.begin(), cs.begin() + (top - 1), cs.end(), std::greater<int64_t>());
+            const int64_t cth = cs[top - 1];
+            for (int64_t i = 0; i < n; i++)
+                if (counts[i] > cth) order.push_back(i);
+            for (int64_t i = 0; i < n && (int64_t)order.size() < top; i++)
+                if (counts[i] == cth) order.push_back(i);
+            std::sort(order.begin(), order.end(),
+                      [&](int64_t a, int64_t b) { return counts[a] != counts[b] ? counts[a] > counts[b] : a < b; });
+        }
         for (int64_t i : order)
             if (!never[i]) eligible_.push_back(i);
         prefix_.assign(eligible_.size() + 1, 0);
@@ -240,7 +256,7 @@ class Quantizer {
     bool run(Quant &q) const
     {
         const int64_t kExhaustive = 96;  // entropy.py:198
-        const int64_t kk_hi = std::min<int64_t>((int64_t)eligible_.size(), k_);
+        const int64_t kk_hi = std::min<int64_t>(n_eligible_, k_);
         Eval best;
         bool have;
         if (kk_hi + 1 <= kExhaustive) {
@@ -269,7 +285,8 @@ class Quantizer {
     const std::vector<int64_t> &counts_;
     int32_t k_, m_, raw_;
     int64_t total_;
-    std::vector<int64_t> eligible_;
+    std::vector<int64_t> eligible_;  // the first min(n_eligible, k + 1) in (-count, index) order
+    int64_t n_eligible_ = 0;
     std::vector<int64_t> prefix_;
     double logk_;
     std::vector<double> lg_;

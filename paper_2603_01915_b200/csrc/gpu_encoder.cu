@@ -23,6 +23,9 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -320,17 +323,20 @@ __global__ void __launch_bounds__(256) emit_pass(const Args a)
     }
 }
 
-// Device buffers of one encode, freed on every exit path.
+// Device buffers of one encode, freed on every exit path.  Stream-ordered
+// allocations from the device's default memory pool, which keeps freed
+// memory (release threshold raised once), so repeated encodes and the
+// scratch of the sort do not pay cudaMalloc/cudaFree each time.
 struct Buffers {
     std::vector<void *> ptrs;
     ~Buffers()
     {
-        for (void *p : ptrs) cudaFree(p);
+        for (void *p : ptrs) cudaFreeAsync(p, 0);
     }
     template <typename T> cudaError_t alloc(T **p, size_t count)
     {
         void *q = nullptr;
-        const cudaError_t e = cudaMalloc(&q, std::max<size_t>(count, 1) * sizeof(T));
+        const cudaError_t e = cudaMallocAsync(&q, std::max<size_t>(count, 1) * sizeof(T), 0);
         if (e == cudaSuccess) ptrs.push_back(q);
         *p = (T *)q;
         return e;
@@ -414,6 +420,29 @@ int upload_domain(Buffers &B, const Domain &D, DevDomain &dd, dtans_encoded *out
 using namespace dtans;
 using namespace dtans::genc;
 
+namespace {
+// DTANS_VERBOSE: per-phase wall times of the GPU encoder.
+struct PhaseTimer {
+    bool on = getenv("DTANS_VERBOSE") != nullptr;
+    std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+    char buf[512] = {0};
+    size_t len = 0;
+    void mark(const char *what)
+    {
+        if (!on) return;
+        cudaDeviceSynchronize();
+        const auto now = std::chrono::steady_clock::now();
+        len += (size_t)snprintf(buf + len, sizeof(buf) - len, " %s %.3f", what,
+                                std::chrono::duration<double>(now - t).count());
+        t = now;
+    }
+    ~PhaseTimer()
+    {
+        if (on) fprintf(stderr, "[dtans] encode_device (s):%s\n", buf);
+    }
+};
+}  // namespace
+
 extern "C" int dtans_encode_device(const dtans_csr_view *m, const dtans_encode_opts *opts, int device,
                                    dtans_encoded *out)
 {
@@ -439,6 +468,14 @@ extern "C" int dtans_encode_device(const dtans_csr_view *m, const dtans_encode_o
     GK(cudaSetDevice(device), "cudaSetDevice");
     int sms = 0;
     GK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device), "sm count");
+    {
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+            uint64_t keep = ~0ull;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+        }
+    }
+    PhaseTimer pt;
     Buffers B;
     Args a{};
     a.rows = rows;
@@ -460,6 +497,7 @@ extern "C" int dtans_encode_device(const dtans_csr_view *m, const dtans_encode_o
         GK(cudaMemcpy(vals, m->values, (size_t)nnz * prec, cudaMemcpyHostToDevice), "upload");
     }
     GK(cudaMemset(head, 0, std::max<int64_t>(nnz, 1)), "memset");
+    pt.mark("upload");
     GK(cudaMemset(err, 0, sizeof(unsigned int)), "memset");
     a.row_start = rs;
     a.col = col;
@@ -488,6 +526,7 @@ extern "C" int dtans_encode_device(const dtans_csr_view *m, const dtans_encode_o
         if (herr & kErrRowStart) return fail(DTANS_E_PARAM, "row_start must be nondecreasing");
         if (herr & kErrColRange) return fail(DTANS_E_PARAM, "column index out of range");
         if (herr & kErrColOrder) return fail(DTANS_E_PARAM, "columns must be strictly ascending per row");
+        pt.mark("extract");
         // 2. distributions (container.py:112-114)
         int rc = distribution<uint32_t>(E, dkey, nnz, ddist, out);
         if (rc) return rc;
@@ -495,6 +534,7 @@ extern "C" int dtans_encode_device(const dtans_csr_view *m, const dtans_encode_o
                        : distribution<uint32_t>(E, reinterpret_cast<uint32_t *>(vkey), nnz, vdist, out);
         if (rc) return rc;
     }
+    pt.mark("distributions");
     // 3. quantize + tables on the host
     const int rec = prec == 8 ? 16 : 12;
     out->tables = (uint8_t *)malloc((size_t)kK * rec);
@@ -512,6 +552,7 @@ extern "C" int dtans_encode_device(const dtans_csr_view *m, const dtans_encode_o
             return rc;
         }
     }
+    pt.mark("quantize+tables");
     for (int64_t i = 0; i < rows; i++) out->row_symbols[i] = (uint32_t)(2 * (m->row_start[i + 1] - m->row_start[i]));
     out->rows = rows;
     out->cols = m->cols;
@@ -558,6 +599,7 @@ extern "C" int dtans_encode_device(const dtans_csr_view *m, const dtans_encode_o
         return fail(DTANS_E_CODING, "symbol not retained and its table has no escape entry");
     }
     const int64_t nwords = (int64_t)out->directory[nslices];
+    pt.mark("base+scan");
     // 6. digit pass + interleave
     uint32_t *stream;
     GK(B.alloc(&stream, nwords), "cudaMalloc");
@@ -565,6 +607,7 @@ extern "C" int dtans_encode_device(const dtans_csr_view *m, const dtans_encode_o
     a.stream = stream;
     emit_pass<<<egrid, 256, smem>>>(a);
     GK(cudaGetLastError(), "launch");
+    pt.mark("emit");
     out->stream = (uint32_t *)malloc(sizeof(uint32_t) * (size_t)std::max<int64_t>(nwords, 1));
     if (!out->stream) {
         dtans_encoded_free(out);
@@ -577,5 +620,6 @@ extern "C" int dtans_encode_device(const dtans_csr_view *m, const dtans_encode_o
         return fail(DTANS_E_CORRUPT, "GPU encoder: slice word accounting mismatch");
     }
     out->nwords = nwords;
+    pt.mark("download");
     return DTANS_OK;
 }

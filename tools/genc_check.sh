@@ -1,7 +1,7 @@
 #!/bin/bash
 # GPU encoder parity + timing against the host encoder.
 python -m pytest tests/test_gpu_encoder.py -x -q 2>&1 | tail -15
-python - <<'PY'
+DTANS_VERBOSE=1 python - <<'PY'
 import time, numpy as np, paper_2603_01915_b200 as P
 from paper_2603_01915_b200 import synth
 for name, gen in [("laplacian g=2591 (2^25 nnz)", lambda: synth.laplacian_2d(2591)),
