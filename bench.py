@@ -283,6 +283,8 @@ def main():
     ap.add_argument("--impl", default="dtans", choices=["dtans", "reference"])
     ap.add_argument("--config", default="laplacian")
     ap.add_argument("--scale", type=float, default=1.0)
+    ap.add_argument("--no-device-encode", action="store_true",
+                    help="skip timing the GPU encoder (encode_matrix(device=)) next to the host encoder")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-cusparse", action="store_true")
     ap.add_argument("--reorder", nargs="?", const="rows", default=None, choices=["rows", "sym"],
@@ -339,6 +341,14 @@ def main():
         c = P.encode_matrix(m)
         cfg["row_order"] = "natural"
     t_enc = time.time() - t0
+    if not args.reorder and not args.no_device_encode:
+        # the GPU encoder (dtans_encode_device) on the same matrix: its time,
+        # and that its container is the host encoder's, byte for byte
+        t0 = time.time()
+        cd = P.encode_matrix(m, device=local)
+        cfg["encode_device_s"] = time.time() - t0
+        cfg["encode_device_identical"] = bool(cd == c)
+        del cd
     x, y = synth.vectors(m)
     V = np.float64 if c.precision == 8 else np.float32
     esz = c.precision
