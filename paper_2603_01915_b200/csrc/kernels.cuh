@@ -358,38 +358,49 @@ __device__ __forceinline__ void lookup_pair(const Ctx &C, uint32_t sod, uint32_t
 //   at most one payload word: its rank among the escaping lanes; f64 value
 //   escapes never qualify), 2 = general case.
 template <typename T>
-__device__ __forceinline__ int payload_probe(const Ctx &C, const bool act, const uint32_t e[8])
+__device__ __forceinline__ int payload_probe(const Ctx &C, const bool act, const uint32_t e[8], bool &dany)
 {
     const uint32_t FULL = 0xFFFFFFFFu;
     // cheap test first: escape entries are the largest entries of a table
-    const uint32_t dmax = max(max(e[0], e[2]), max(e[4], e[6]));
+    const uint32_t m02 = max(e[0], e[2]), m46 = max(e[4], e[6]);
+    const uint32_t dmax = max(m02, m46);
     const uint32_t vmax = max(max(e[1], e[3]), max(e[5], e[7]));
-    const bool dany = act && dmax >= C.desc_min;
+    dany = act && dmax >= C.desc_min;
     const bool vany = act && vmax >= C.vesc_min;
     if (!__any_sync(FULL, dany || vany)) return 0;
-    const bool d0 = e[0] >= C.desc_min, d1 = e[2] >= C.desc_min, d2 = e[4] >= C.desc_min, d3 = e[6] >= C.desc_min;
-    const bool dmulti = (d0 && (d1 || d2 || d3)) || (d1 && (d2 || d3)) || (d2 && d3);
     bool fast;
     if (T::kPayloadWords == 2) {
-        fast = !vany && !dmulti;
+        // f64: no value escape, and at most one delta escape per lane, i.e.
+        // the second-largest delta entry does not escape
+        const uint32_t d2 = max(max(min(e[0], e[2]), min(e[4], e[6])), min(m02, m46));
+        fast = !vany && !(act && d2 >= C.desc_min);
     } else {
+        const bool d0 = e[0] >= C.desc_min, d1 = e[2] >= C.desc_min, d2 = e[4] >= C.desc_min,
+                   d3 = e[6] >= C.desc_min;
+        const bool dmulti = (d0 && (d1 || d2 || d3)) || (d1 && (d2 || d3)) || (d2 && d3);
         const bool v0 = e[1] >= C.vesc_min, v1 = e[3] >= C.vesc_min, v2 = e[5] >= C.vesc_min,
                    v3 = e[7] >= C.vesc_min;
         const bool vmulti = (v0 && (v1 || v2 || v3)) || (v1 && (v2 || v3)) || (v2 && v3);
-        fast = !(dmulti || vmulti || (dany && vany));
+        fast = !act || !(dmulti || vmulti || (dany && vany));
     }
-    return __all_sync(FULL, !act || fast) ? 1 : 2;
+    return __all_sync(FULL, fast) ? 1 : 2;
 }
 
+// Fast payload event: every lane reads at most one word, at its rank among
+// the escaping lanes.  f64 (kPayloadWords == 2): only a delta can escape
+// here, so `dany` (from the probe) is the lane's escape flag.
 template <typename T, class Src>
 __device__ __forceinline__ void payload_fast(const Ctx &C, const Src &src, uint32_t &cur, const bool act,
-                                             const uint32_t e[8], uint32_t ds[4], typename T::Bits vs[4])
+                                             const bool dany, const uint32_t e[8], uint32_t ds[4],
+                                             typename T::Bits vs[4])
 {
     using Bits = typename T::Bits;
-    bool esc = false;
+    bool esc = dany;
+    if (T::kPayloadWords == 1) {
 #pragma unroll
-    for (int k = 0; k < 8; k++) esc = esc || e[k] >= ((k & 1) ? C.vesc_min : C.desc_min);
-    const uint32_t m = __ballot_sync(0xFFFFFFFFu, act && esc);
+        for (int k = 1; k < 8; k += 2) esc = esc || (act && e[k] >= C.vesc_min);
+    }
+    const uint32_t m = __ballot_sync(0xFFFFFFFFu, esc);
     const uint32_t w = src(cur + __popc(m & C.lt));
     cur += __popc(m);
 #pragma unroll
@@ -447,8 +458,9 @@ template <typename T, class Src>
 __device__ __forceinline__ void payload_event(const Ctx &C, const Src &src, uint32_t &cur, const bool act,
                                               const uint32_t e[8], uint32_t ds[4], typename T::Bits vs[4])
 {
-    const int pk = payload_probe<T>(C, act, e);
-    if (pk == 1) payload_fast<T>(C, src, cur, act, e, ds, vs);
+    bool dany;
+    const int pk = payload_probe<T>(C, act, e, dany);
+    if (pk == 1) payload_fast<T>(C, src, cur, act, dany, e, ds, vs);
     else if (pk == 2) payload_slow<T>(C, src, cur, act, e, ds, vs);
 }
 
@@ -567,13 +579,14 @@ __device__ __forceinline__ void full_segment(const KernelArgs &a, const Ctx &C, 
             }
         }
     };
-    const int pk = payload_probe<T>(C, act, e);
+    bool dany;
+    const int pk = payload_probe<T>(C, act, e, dany);
     if (pk == 2) {
         payload_slow<T>(C, src, cur, act, e, ds, vs);
         rest(ds, vs);
         return;
     }
-    if (pk == 1) payload_fast<T>(C, src, cur, act, e, ds, vs);
+    if (pk == 1) payload_fast<T>(C, src, cur, act, dany, e, ds, vs);
     rest(ds, vs);
 }
 
