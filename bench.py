@@ -152,7 +152,12 @@ def dist_setup(gpus: int):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl")
+        # DTANS_DIST_BACKEND=gloo + DTANS_SHARE_GPU=1: exercise the N>1 path
+        # with several ranks on one GPU (a test of the plumbing, not a bench)
+        dist.init_process_group(os.environ.get("DTANS_DIST_BACKEND", "nccl"))
+        if os.environ.get("DTANS_SHARE_GPU") == "1":
+            import torch
+            local = local % max(1, torch.cuda.device_count())
     return world, rank, local
 
 
