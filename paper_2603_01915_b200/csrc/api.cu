@@ -830,7 +830,8 @@ extern "C" int dtans_spmv_host(dtans_dev *h, const void *x, const void *y, void 
     const int64_t nchunks = (int64_t)h->chunks.size();
     const char *eh = getenv("DTANS_HOST_STAGES");
     const int stages = std::max(1, std::min(kHostChunks, eh ? atoi(eh) : 8));
-    const bool chunked = h->base.nlong == 0 && !h->base.dynamic && nchunks >= 64 * stages;
+    // y/out ranges are contiguous only in natural row order (no row map)
+    const bool chunked = h->base.nlong == 0 && !h->base.dynamic && nchunks >= 64 * stages && !h->d_row_map;
     if (!h->st_in) {
         CK(cudaStreamCreateWithFlags(&h->st_in, cudaStreamNonBlocking), "stream");
         CK(cudaStreamCreateWithFlags(&h->st_comp, cudaStreamNonBlocking), "stream");
