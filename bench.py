@@ -243,7 +243,21 @@ def run_powerit(args, world, rank, local):
     del m
     op = D.ShardedSpMV.from_local(c, rows_of, rank, world, device=dev)
     x0 = torch.full((n,), 1.0 / np.sqrt(n), dtype=torch.float64, device=dev)
-    D.power_iteration(op, x0, args.warmup)
+    if args.driver == "capi":
+        # the C-ABI driver: dtans_mg_power_iteration (NCCL all-reduce +
+        # grouped broadcasts into each shard's offset, one call per run)
+        if world > 1:
+            comm = D.NcclComm.from_torch(local)
+        else:
+            comm = D.NcclComm(1, 0, local, D.NcclComm.unique_id())
+        row_off = [r0 for r0, _ in rows_of] + [rows_of[-1][1]]
+
+        def run_iters(k):
+            return comm.power_iteration(op._dev, row_off, x0, k)
+    else:
+        def run_iters(k):
+            return D.power_iteration(op, x0, k)
+    run_iters(args.warmup)
     iters = args.steps
     barrier(world)
     torch.cuda.synchronize()
@@ -251,7 +265,7 @@ def run_powerit(args, world, rank, local):
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record()
-        x, lam = D.power_iteration(op, x0, iters)
+        x, lam = run_iters(iters)
         e1.record()
         torch.cuda.synchronize()
     barrier(world)
@@ -269,7 +283,10 @@ def run_powerit(args, world, rank, local):
            "data": "synthetic",
            "config": {"workload": "power iteration, banded-32 positive alphabet, BASELINE configs[4]",
                       "rows": n, "nnz": int(nnz_total), "parallelism": f"row shards x{world}",
-                      "collectives": "all_reduce(1 f64) + all_gather_into_tensor(y) per iteration (NCCL)",
+                      "collectives": ("all_reduce(1 f64) + grouped ncclBroadcast of every shard's y per "
+                                      "iteration (dtans_mg_power_iteration, C ABI)" if args.driver == "capi" else
+                                      "all_reduce(1 f64) + all_gather_into_tensor(y) per iteration (NCCL)"),
+                      "driver": args.driver,
                       "encode_s": t_enc},
            "lambda": lam,
            "roofline": {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
@@ -288,6 +305,8 @@ def main():
     ap.add_argument("--impl", default="dtans", choices=["dtans", "reference"])
     ap.add_argument("--config", default="laplacian")
     ap.add_argument("--scale", type=float, default=1.0)
+    ap.add_argument("--driver", default="torch", choices=["torch", "capi"],
+                    help="power iteration: torch.distributed loop, or the C-ABI NCCL driver")
     ap.add_argument("--no-device-encode", action="store_true",
                     help="skip timing the GPU encoder (encode_matrix(device=)) next to the host encoder")
     ap.add_argument("--no-cpu-baseline", action="store_true")

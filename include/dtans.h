@@ -148,6 +148,29 @@ int dtans_spmv_f32(dtans_dev *h, const float *x, const float *y, float *out,
 int dtans_spmv_scaled(dtans_dev *h, const void *x, void *out, const double *sumsq_in,
                       double *sumsq_out, double *sumsq_zero, void *stream);
 
+/* ------------------------------------------------------------------ */
+/* Multi-GPU (NCCL over NVLink/NVSwitch; one process per GPU).  NCCL is
+ * loaded at run time (libnccl.so.2); without it these return
+ * DTANS_E_NODEVICE.  No reference counterpart: the reference is one CPU
+ * process; this is the SURVEY §8b/§8e power-iteration driver. */
+typedef struct dtans_mg dtans_mg; /* opaque: one NCCL communicator */
+
+/* ncclGetUniqueId into id[128] (rank 0; share the bytes with every rank). */
+int dtans_mg_unique_id(uint8_t *id);
+/* ncclCommInitRank on CUDA device `device`. */
+int dtans_mg_init(const uint8_t *id, int nranks, int rank, int device, dtans_mg **out);
+void dtans_mg_free(dtans_mg *g);
+
+/* Power iteration x <- A x / ||A x||_2 over row shards: this rank's handle
+ * h holds rows [row_off[rank], row_off[rank+1]) of a square n x n matrix,
+ * n = row_off[nranks] (distributed.shard).  x (device, n values, container
+ * precision) holds x0 on entry, the same on every rank, and x_iters on exit;
+ * *lambda_out = ||A x_{iters-1}||.  Per iteration: the fused scaled SpMV,
+ * ncclAllReduce of sum(y^2) (one f64) and grouped ncclBroadcasts of every
+ * shard's y into its row offset of the next x, all on `stream`. */
+int dtans_mg_power_iteration(dtans_mg *g, dtans_dev *h, const int64_t *row_off, void *x, int iters,
+                             double *lambda_out, void *stream);
+
 /* Same product with HOST x, y, out (pageable or pinned): H2D copy, kernel,
  * D2H copy, synchronize, consumption check.  The end-to-end entry point a
  * ctypes binding of spmv(c, x, y) calls. */

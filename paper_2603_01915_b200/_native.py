@@ -25,7 +25,7 @@ EXPORTS = (
     "dtans_quantize", "dtans_upload", "dtans_free", "dtans_info", "dtans_spmv_f64",
     "dtans_spmv_f32", "dtans_spmv_host", "dtans_decode", "dtans_check",
     "dtans_launch_count", "dtans_set_row_map", "dtans_spmv_scaled", "dtans_set_col_map",
-    "dtans_encode_device",
+    "dtans_encode_device", "dtans_mg_unique_id", "dtans_mg_init", "dtans_mg_free", "dtans_mg_power_iteration",
 )
 
 
@@ -83,6 +83,11 @@ def lib() -> ctypes.CDLL:
     L.dtans_encode.argtypes = [ctypes.POINTER(CsrView), ctypes.POINTER(EncodeOpts), ctypes.POINTER(Encoded)]
     L.dtans_encode_device.argtypes = [ctypes.POINTER(CsrView), ctypes.POINTER(EncodeOpts), ctypes.c_int,
                                       ctypes.POINTER(Encoded)]
+    L.dtans_mg_unique_id.argtypes = [vp]
+    L.dtans_mg_init.argtypes = [vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.POINTER(vp)]
+    L.dtans_mg_free.argtypes = [vp]
+    L.dtans_mg_free.restype = None
+    L.dtans_mg_power_iteration.argtypes = [vp, vp, vp, vp, ctypes.c_int, ctypes.POINTER(ctypes.c_double), vp]
     L.dtans_encoded_free.argtypes = [ctypes.POINTER(Encoded)]
     L.dtans_encoded_free.restype = None
     L.dtans_quantize.argtypes = [i64, vp, vp, i32, i32, i32, i64, vp, vp, vp, vp]

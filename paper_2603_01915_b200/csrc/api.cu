@@ -54,6 +54,15 @@ struct dtans_dev {
     cudaEvent_t ev_in[kHostChunks] = {}, ev_done[kHostChunks] = {};
 };
 
+namespace dtans {
+void dev_shape(const dtans_dev *h, int64_t *rows, int64_t *cols, int32_t *precision)
+{
+    *rows = h->rows;
+    *cols = h->cols;
+    *precision = h->precision;
+}
+}  // namespace dtans
+
 namespace {
 
 int cuda_fail(cudaError_t e, const char *what)

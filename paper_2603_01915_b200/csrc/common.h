@@ -22,6 +22,9 @@ inline int fail(int code, const char *fmt, ...)
     return code;
 }
 
+// Shape of an uploaded container (api.cu; used by the multi-GPU driver mg.cu).
+void dev_shape(const dtans_dev *h, int64_t *rows, int64_t *cols, int32_t *precision);
+
 constexpr int kSlice = 32;     // rows per slice = lanes per warp (container.py:45)
 constexpr int kK = 4096;       // table slots
 constexpr int kKLog2 = 12;

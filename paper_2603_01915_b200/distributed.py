@@ -226,6 +226,70 @@ def _power_iteration_fused(op: ShardedSpMV, x0, iters: int, group=None):
     return x, float(norm.item())
 
 
+class NcclComm:
+    """An NCCL communicator owned by libdtans (``dtans_mg_init``): one per
+    process / GPU.  ``unique_id`` comes from ``NcclComm.unique_id()`` on rank
+    0 and is shared with the other ranks by any means (``from_torch`` uses a
+    torch.distributed broadcast)."""
+
+    def __init__(self, nranks: int, rank: int, device: int, unique_id: bytes):
+        import ctypes
+        from . import _native
+        if len(unique_id) != 128:
+            raise ParameterError("an NCCL unique id has 128 bytes")
+        self._L = _native.lib()
+        buf = (ctypes.c_uint8 * 128).from_buffer_copy(unique_id)
+        h = ctypes.c_void_p()
+        _native.check(self._L.dtans_mg_init(ctypes.addressof(buf), nranks, rank, device, ctypes.byref(h)))
+        self.handle, self.nranks, self.rank, self.device = h, nranks, rank, device
+
+    @staticmethod
+    def unique_id() -> bytes:
+        import ctypes
+        from . import _native
+        buf = (ctypes.c_uint8 * 128)()
+        _native.check(_native.lib().dtans_mg_unique_id(ctypes.addressof(buf)))
+        return bytes(buf)
+
+    @classmethod
+    def from_torch(cls, device: int, group=None) -> "NcclComm":
+        """Rank 0 makes the id; torch.distributed broadcasts it."""
+        import torch.distributed as dist
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+        obj = [cls.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0, group=group)
+        return cls(world, rank, device, obj[0])
+
+    def power_iteration(self, dev, row_off, x0, iters: int, stream=None):
+        """dtans_mg_power_iteration: ``dev`` is this rank's DeviceContainer
+        (rows [row_off[rank], row_off[rank+1]) of a square matrix), ``x0`` a
+        full-length CUDA tensor in the container precision, the same on every
+        rank.  Returns (x_iters, lambda) like ``power_iteration``."""
+        import ctypes
+        import torch
+        from . import _native
+        ro = np.ascontiguousarray(row_off, dtype=np.int64)
+        if len(ro) != self.nranks + 1:
+            raise ParameterError("row_off needs nranks + 1 entries")
+        x = x0.detach().clone().contiguous()
+        lam = ctypes.c_double(float("nan"))
+        st = torch.cuda.current_stream(x.device).cuda_stream if stream is None else stream
+        _native.check(self._L.dtans_mg_power_iteration(self.handle, dev.handle, ro.ctypes.data, x.data_ptr(),
+                                                       int(iters), ctypes.byref(lam), st))
+        return x, lam.value
+
+    def close(self):
+        if getattr(self, "handle", None):
+            self._L.dtans_mg_free(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # pragma: no cover - interpreter shutdown
+            pass
+
+
 def reference_power_iteration(A_csr, x0: np.ndarray, iters: int):
     """Plain numpy power iteration on a CSR matrix (test checker)."""
     import scipy.sparse as sp

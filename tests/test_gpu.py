@@ -239,3 +239,42 @@ def test_host_buffer_path_row_reordered():
     x, y = synth.vectors(m)
     out, ref = _host_vs_device(c, x, y)
     assert np.array_equal(out, ref)
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_nccl_power_iteration_c_abi(dtype):
+    """dtans_mg_power_iteration (NCCL all-reduce + grouped broadcasts in the
+    C ABI) on a one-rank communicator matches the torch-driven fused power
+    iteration and the numpy reference.  Not bitwise: sum(y^2) is accumulated
+    with per-warp f64 atomics, whose order varies from run to run."""
+    from paper_2603_01915_b200 import distributed as D
+    m = synth.banded(20000, 32, positive=True, seed=3)
+    if dtype == np.float32:
+        m = P.CsrMatrix(m.rows, m.cols, m.row_start, m.col_idx, m.values.astype(np.float32))
+    c = P.encode_matrix(m)
+    op = D.ShardedSpMV(c, 0, 1, device=torch.device("cuda", 0))
+    tdt = torch.float64 if dtype == np.float64 else torch.float32
+    x0 = torch.full((m.cols,), 1.0 / np.sqrt(m.cols), dtype=tdt, device="cuda")
+    x_t, lam_t = D.power_iteration(op, x0, 25)
+    comm = D.NcclComm(1, 0, 0, D.NcclComm.unique_id())
+    x_c, lam_c = comm.power_iteration(op._dev, [0, m.rows], x0, 25)
+    torch.cuda.synchronize()
+    tol = 1e-12 if dtype == np.float64 else 1e-5
+    assert abs(lam_c - lam_t) <= tol * lam_t
+    assert torch.allclose(x_c, x_t, rtol=10 * tol, atol=0)
+    xr, lr = D.reference_power_iteration(m, np.full(m.cols, 1.0 / np.sqrt(m.cols)), 25)
+    assert abs(lam_c - lr) <= tol * lr
+    assert np.allclose(x_c.double().cpu().numpy(), xr, rtol=100 * tol, atol=1e-14 if dtype == np.float64 else 1e-7)
+    comm.close()
+
+
+def test_nccl_power_iteration_rejects_bad_layout():
+    from paper_2603_01915_b200 import distributed as D
+    m = synth.banded(5000, 8, positive=True, seed=1)
+    c = P.encode_matrix(m)
+    dev = c.device(0)
+    comm = D.NcclComm(1, 0, 0, D.NcclComm.unique_id())
+    x0 = torch.ones(m.cols, dtype=torch.float64, device="cuda")
+    with pytest.raises(P.ParameterError):
+        comm.power_iteration(dev, [0, m.rows - 1], x0, 3)
+    comm.close()
