@@ -42,6 +42,9 @@ struct dtans_dev {
     void *d_long = nullptr;     // tasks + pool + slices + partials
     size_t long_bytes = 0;
     int task_ctas = 0, task_smem = 0, solo_ctas = 0, solo_smem = 0;
+    // CTA-pipelined main kernel (dtans_cta_kernel): ring of cta_stages buffers of cta_bufb bytes
+    bool cta_mode = false;
+    int cta_stages = 0, cta_bufb = 0, cta_smem = 0;
     uint32_t *d_row_map = nullptr;  // optional output row map (reordered P*A)
     uint32_t *d_col_map = nullptr;  // optional column map (symmetric P*A*P^T): x'[j] = x[map[j]]
     void *d_xperm = nullptr;        // x' scratch (cols values)
@@ -263,6 +266,16 @@ int with_kernel(bool dinline, F &&f)
 }
 
 template <typename V, class F>
+int with_cta_kernel(bool dinline, F &&f)
+{
+    if (dinline)
+        return f(dev::dtans_cta_kernel<V, false, true, true>, dev::dtans_cta_kernel<V, false, false, true>,
+                 dev::dtans_cta_kernel<V, true, false, true>, dev::dtans_cta_kernel<V, false, false, true, true>);
+    return f(dev::dtans_cta_kernel<V, false, true, false>, dev::dtans_cta_kernel<V, false, false, false>,
+             dev::dtans_cta_kernel<V, true, false, false>, dev::dtans_cta_kernel<V, false, false, false, true>);
+}
+
+template <typename V, class F>
 int with_long_kernels(bool dinline, F &&f)
 {
     if (dinline)
@@ -343,6 +356,17 @@ int configure(dtans_dev *h, const TableBlock &tb, const SmemPlan &sp)
     });
     if (rc) return rc;
     if (per_sm < 1) return fail(DTANS_E_CUDA, "kernel does not fit on an SM");
+    if (h->cta_mode) {
+        a.nstages = h->cta_stages;
+        rc = with_cta_kernel<V>(tb.dinline, [&](auto k0, auto k1, auto k2, auto k3) -> int {
+            CK(cudaFuncSetAttribute(k0, cudaFuncAttributeMaxDynamicSharedMemorySize, h->cta_smem), "attr");
+            CK(cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, h->cta_smem), "attr");
+            CK(cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, h->cta_smem), "attr");
+            CK(cudaFuncSetAttribute(k3, cudaFuncAttributeMaxDynamicSharedMemorySize, h->cta_smem), "attr");
+            return DTANS_OK;
+        });
+        if (rc) return rc;
+    }
     return DTANS_OK;
 }
 
@@ -387,7 +411,24 @@ int launch(dtans_dev *h, const V *x, const V *y, V *out, const int64_t *row_star
     a.sumsq_in = sumsq_in;
     a.sumsq_out = sumsq_out;
     a.sumsq_zero = sumsq_zero;
-    if (nch > 0) {
+    if (nch > 0 && h->cta_mode) {
+        dev::KernelArgs b = a;
+        b.bufb = h->cta_bufb;
+        b.nstages = h->cta_stages;
+        const int cctas = (int)std::max<int64_t>(1, std::min<int64_t>(h->sms, nch));
+        with_cta_kernel<V>(h->dinline, [&](auto kspmv, auto kspmv0, auto kdec, auto kscaled) -> int {
+            if (scaled)
+                kscaled<<<cctas, h->threads, h->cta_smem, st>>>(b);
+            else if (decode_only)
+                kdec<<<cctas, h->threads, h->cta_smem, st>>>(b);
+            else if (y != nullptr)
+                kspmv<<<cctas, h->threads, h->cta_smem, st>>>(b);
+            else
+                kspmv0<<<cctas, h->threads, h->cta_smem, st>>>(b);
+            return 0;
+        });
+        h->launches++;
+    } else if (nch > 0) {
         with_kernel<V>(h->dinline, [&](auto kspmv, auto kspmv0, auto kdec, auto kscaled) -> int {
             if (scaled)
                 kscaled<<<ctas, h->threads, h->smem, st>>>(a);
@@ -539,6 +580,19 @@ extern "C" int dtans_upload(const dtans_container_view *c, int device, dtans_dev
             std::stable_sort(order.begin(), order.end(), [&](uint32_t p, uint32_t q) { return cost[p] > cost[q]; });
             for (uint32_t s : order) push(s, 1);
         } else {
+            // CTA-pipelined kernel (DTANS_CTA=1): chunks of up to kCtaConsumers
+            // slices (one per consumer warp) in a CTA ring of >= 3 stages
+            const char *ec = getenv("DTANS_CTA");
+            const char *es = getenv("DTANS_CTA_STAGES");
+            const int64_t nst = es ? std::max(2, std::min(atoi(es), dev::kMaxCtaStages)) : 6;
+            const int64_t space = (int64_t)max_optin - sp.off_bufs - dev::kOverrunWords * 4;
+            const int64_t bb = space / nst / 16 * 16;  // stage bytes
+            if (!dyn && ec && atoi(ec) != 0 && bb >= (int64_t)sp.bufb && bb / 4 < 65536) {
+                h->cta_mode = true;
+                h->cta_stages = (int)nst;
+                h->cta_bufb = (int)bb;
+                h->cta_smem = (int)(sp.off_bufs + nst * bb + dev::kOverrunWords * 4);
+            }
             int64_t s = 0;
             while (s < nsl) {
                 if (is_long[s]) {
@@ -546,9 +600,15 @@ extern "C" int dtans_upload(const dtans_container_view *c, int device, dtans_dev
                     continue;
                 }
                 int64_t k = 1;
-                while (k < kcap && s + k < nsl && !is_long[s + k] &&
-                       chunk_bytes(c->directory, s, k + 1) <= (uint64_t)sp.bufb)
-                    k++;
+                if (h->cta_mode) {
+                    while (k < dev::kCtaConsumers && s + k < nsl && !is_long[s + k] &&
+                           chunk_bytes(c->directory, s, k + 1) <= (uint64_t)h->cta_bufb)
+                        k++;
+                } else {
+                    while (k < kcap && s + k < nsl && !is_long[s + k] &&
+                           chunk_bytes(c->directory, s, k + 1) <= (uint64_t)sp.bufb)
+                        k++;
+                }
                 push(s, k);
                 s += k;
             }
@@ -680,9 +740,10 @@ extern "C" int dtans_upload(const dtans_container_view *c, int device, dtans_dev
     if (getenv("DTANS_VERBOSE"))
         fprintf(stderr,
                 "[dtans] rows=%lld slices=%lld chunks=%zu nring=%d bufb=%d smem=%d dinline=%d rep_d=%d rep_v=%d "
-                "nlong=%u ntasks=%u nsolo=%u dynamic=%d task_smem=%d\n",
+                "nlong=%u ntasks=%u nsolo=%u dynamic=%d task_smem=%d cta_stages=%d cta_bufb=%d\n",
                 (long long)h->rows, (long long)nsl, h->chunks.size(), sp.nring, sp.bufb, h->smem, (int)tb.dinline,
-                tb.rep_d, tb.rep_v, h->base.nlong, h->base.ntasks, h->base.nsolo, h->base.dynamic, h->task_smem);
+                tb.rep_d, tb.rep_v, h->base.nlong, h->base.ntasks, h->base.nsolo, h->base.dynamic, h->task_smem,
+                h->cta_mode ? h->cta_stages : 0, h->cta_bufb);
     *out = h;
     return DTANS_OK;
 }

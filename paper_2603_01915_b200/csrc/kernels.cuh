@@ -144,6 +144,7 @@ struct KernelArgs {
     uint32_t chunk_lo, chunk_hi;  // chunks of this launch
     int32_t dynamic;              // 1: atomic ticket counter instead of a static stride
     uint32_t *work_counter;       // zeroed before every dynamic launch
+    int32_t nstages;              // CTA-pipelined kernel: stage buffers of bufb bytes in the CTA ring
 };
 
 __device__ __forceinline__ uint32_t lanemask_lt()
@@ -913,6 +914,102 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) dtans_kernel(const KernelAr
             b = 0;
             parity ^= 1u;
         }
+    }
+    if (kScaled && a.sumsq_out != nullptr) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) wsum = __dadd_rn(wsum, __shfl_xor_sync(0xFFFFFFFFu, wsum, o));
+        if (lane == 0) atomicAdd(a.sumsq_out, wsum);
+    }
+}
+
+// CTA-pipelined variant of the main kernel: one producer warp (lane 0)
+// stages whole chunks of up to kCtaConsumers slices into a ring of
+// `nstages` CTA-wide buffers with one bulk copy each; the consumer warps
+// deal the chunks' slices round-robin.  Per slice the consumers pay a few
+// shared loads, and per stage one mbarrier wait and one arrive, instead of a
+// per-warp claim/stage pipeline per few slices.
+// Full barriers: the producer's arrive.expect_tx + the copy's complete_tx.
+// Empty barriers: one arrive per consumer warp.  The producer ends the
+// sequence with an empty chunk (k = 0) that every consumer reads as "done".
+constexpr int kCtaConsumers = kMaxWarps - 1;
+constexpr int kMaxCtaStages = kMaxWarps * kMaxRing / 2;  // full + empty barriers fit the bars region
+
+template <typename V, bool kDecode, bool kHasY, bool kDIn, bool kScaled = false>
+__global__ void __launch_bounds__(kMaxWarps * 32, 1) dtans_cta_kernel(const KernelArgs a)
+{
+    const bool aligned = load_tables(a);
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    const uint32_t sb = smem_u32(dtans_smem);
+    const uint32_t S = (uint32_t)a.nstages;
+    const uint32_t full = sb + (uint32_t)a.off_bars, empty = full + 8u * kMaxCtaStages;
+    const uint32_t metas = sb + (uint32_t)a.off_meta;
+    const uint32_t bufs = sb + (uint32_t)a.off_bufs;
+    if (threadIdx.x == 0) {
+        for (uint32_t q = 0; q < S; q++) {
+            mbar_init(full + 8u * q, 1);
+            mbar_init(empty + 8u * q, kCtaConsumers);
+        }
+        fence_mbar_init();
+    }
+    __syncthreads();
+    if (!aligned) {
+        if (threadIdx.x == 0) atomicOr(a.err, 4u);
+        return;
+    }
+    if (warp == kCtaConsumers) {  // producer
+        if (lane == 0) {
+            for (uint32_t i = 0;; i++) {
+                const uint32_t slot = i % S, use = i / S;
+                if (use > 0) mbar_wait(empty + 8u * slot, (use - 1u) & 1u);
+                const uint32_t c = a.chunk_lo + blockIdx.x + i * gridDim.x;
+                const bool v = c < a.chunk_hi;
+                ChunkRec rc{};
+                if (v) rc = a.chunks[c];
+                stage_chunk(a, v, rc, full + 8u * slot, metas + 8u * slot, bufs + slot * (uint32_t)a.bufb);
+                if (!v) break;
+            }
+        }
+        return;
+    }
+    const Ctx C = make_ctx<V>(a, lane);
+    const V *__restrict__ x = reinterpret_cast<const V *>(a.x);
+    V scale = V(1);
+    double wsum = 0.0;
+    if (kScaled) {
+        if (a.sumsq_in != nullptr) {
+            const double q = *a.sumsq_in;
+            scale = (V)__ddiv_rn(1.0, __dsqrt_rn(q));
+        }
+        if (a.sumsq_zero != nullptr && blockIdx.x == 0 && threadIdx.x == 0) *a.sumsq_zero = 0.0;
+    }
+    // consumer w takes the CTA's slices w, w + kCtaConsumers, ... across the
+    // stage sequence (stages hold k <= kCtaConsumers slices each) and
+    // releases every stage once, when it moves past it
+    uint32_t i = 0, slot = 0, base = 0;
+    mbar_wait(full, 0u);
+    uint2 md = ld_shared_v2(metas);
+    for (uint32_t g = (uint32_t)warp; md.y != 0u; g += kCtaConsumers) {
+        while (g >= base + md.y) {
+            __syncwarp();
+            if (lane == 0) mbar_arrive(empty + 8u * slot);
+            base += md.y;
+            i++;
+            slot = i % S;
+            mbar_wait(full + 8u * slot, (i / S) & 1u);
+            md = ld_shared_v2(metas + 8u * slot);
+            if (md.y == 0u) break;  // uniform: the producer's end marker
+        }
+        if (md.y == 0u) break;
+        const uint32_t k = md.y, w = g - base;
+        const uint32_t buf = bufs + slot * (uint32_t)a.bufb;
+        const uint32_t hw = chunk_hdr_words(k);
+        const uint32_t meta = sh32(buf + 4u * w);
+        const uint32_t dstart = w ? (sh32(buf + 4u * w - 4u) & 0xFFFFu) : 0u;
+        const uint32_t n = sh32(buf + (hw + w * 32u + (uint32_t)lane) * 4u);
+        const SmemSrc src{buf + (hw + k * 32u + dstart) * 4u};
+        decode_slice<V, kDecode, kHasY, kDIn, kScaled>(a, C, x, src, (meta & 0xFFFFu) - dstart, meta, n,
+                                                        (md.x + w) * kSliceRows + (uint32_t)lane, lane, scale, wsum);
     }
     if (kScaled && a.sumsq_out != nullptr) {
 #pragma unroll
