@@ -146,6 +146,71 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
+def cusparse_formats(m, V, xt, yt, steps, dtans_ms):
+    """ms per product of cuSPARSE CSR (ALG1, ALG2), COO and SELL-32 on the
+    same matrix and vectors (tools/cusparse_cmp/libcusparse_cmp.so)."""
+    import ctypes
+    import torch
+    path = os.path.join(REPO, "tools", "cusparse_cmp", "libcusparse_cmp.so")
+    if not os.path.exists(path):
+        return {"error": "tools/cusparse_cmp/libcusparse_cmp.so not built"}
+    try:
+        L = ctypes.CDLL(path)
+        L.cmp_last_error.restype = ctypes.c_char_p
+        L.cmp_spmv_time.argtypes = [ctypes.c_int, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
+                                    ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,
+                                    ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
+                                    ctypes.POINTER(ctypes.c_float)]
+        dev = xt.device
+        esz = np.dtype(V).itemsize
+        rs = np.asarray(m.row_start, dtype=np.int64)
+        lens = np.diff(rs)
+        cols = np.asarray(m.col_idx, dtype=np.int64)
+        vals = np.asarray(m.values, dtype=V)
+        t_rs = torch.from_numpy(rs).to(dev)
+        t_cols = torch.from_numpy(cols).to(dev)
+        t_vals = torch.from_numpy(vals).to(dev)
+        t_rows = torch.from_numpy(np.repeat(np.arange(m.rows, dtype=np.int64), lens)).to(dev)
+        # SELL-32: slice s of width w_s stores element k of row 32s+r at off_s + 32k + r
+        nsl = (m.rows + 31) // 32
+        lp = np.zeros(nsl * 32, dtype=np.int64)
+        lp[: m.rows] = lens
+        width = lp.reshape(nsl, 32).max(axis=1)
+        soff = np.zeros(nsl + 1, dtype=np.int64)
+        np.cumsum(width * 32, out=soff[1:])
+        row = np.repeat(np.arange(m.rows, dtype=np.int64), lens)
+        k = np.arange(m.nnz, dtype=np.int64) - np.repeat(rs[:-1], lens)
+        pos = soff[row // 32] + 32 * k + (row % 32)
+        scol = np.full(int(soff[-1]), -1, dtype=np.int64)
+        sval = np.zeros(int(soff[-1]), dtype=V)
+        scol[pos] = cols
+        sval[pos] = vals
+        del row, k, pos
+        t_soff = torch.from_numpy(soff).to(dev)
+        t_scol = torch.from_numpy(scol).to(dev)
+        t_sval = torch.from_numpy(sval).to(dev)
+        y = yt.clone()
+        res = {"impl": "cusparseSpMV (tools/cusparse_cmp), y = A x + y, mean of the timed products"}
+        iters = max(10, min(steps, 100))
+        specs = [("csr_alg1", 0, t_rs, t_cols, t_vals, 0), ("csr_alg2", 1, t_rs, t_cols, t_vals, 0),
+                 ("coo", 2, t_rows, t_cols, t_vals, 0), ("sell32", 3, t_soff, t_scol, t_sval, int(soff[-1]))]
+        for name, fmt, a0, a1, a2, ssz in specs:
+            msv = ctypes.c_float(0.0)
+            rc = L.cmp_spmv_time(fmt, m.rows, m.cols, m.nnz, a0.data_ptr(), a1.data_ptr(), a2.data_ptr(), ssz,
+                                 esz, xt.data_ptr(), y.data_ptr(), 3, iters, ctypes.byref(msv))
+            if rc:
+                res[name] = {"error": L.cmp_last_error().decode()}
+            else:
+                res[name] = {"ms": msv.value, "gflops": 2 * m.nnz / (msv.value * 1e-3) / 1e9,
+                             "dtans_speedup": msv.value / dtans_ms}
+        best = min((v["ms"] for v in res.values() if isinstance(v, dict) and "ms" in v), default=None)
+        res["best_ms"] = best
+        res["dtans_speedup_vs_best"] = best / dtans_ms if best else None
+        return res
+    except Exception as e:  # comparator only
+        return {"error": str(e)[:200]}
+
+
 def dist_setup(gpus: int):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -476,6 +541,13 @@ def main():
         except Exception as e:  # comparator only
             cus = {"error": str(e)[:200]}
 
+    # cuSPARSE generic SpMV in every format SURVEY 8d names (CSR ALG1/ALG2,
+    # COO, sliced ELL with slice 32), through tools/cusparse_cmp (a comparator
+    # library; the product never links cuSPARSE)
+    cus_fmt = None
+    if not args.no_cusparse and world == 1:
+        cus_fmt = cusparse_formats(m, V, xt, yt, args.steps, ms)
+
     pk, pk_kind = peaks()
     achieved = alg_bytes / (ms_local * 1e-3) / 1e9
     traffic = None
@@ -513,6 +585,7 @@ def main():
                 "h2d_bytes_per_step": esz * (m.cols + m.rows), "d2h_bytes_per_step": esz * m.rows,
                 "path": "dtans_spmv_host (C ABI, pinned host x/y/out)", "matches_device_result": ref_ok},
         "cusparse_csr": cus,
+        "cusparse_formats": cus_fmt,
         "cpu_baseline": cpu,
         "clocks": clk.summary(),
         "gpu_launches": gpu_launches,
