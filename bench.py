@@ -552,9 +552,20 @@ def main():
     achieved = alg_bytes / (ms_local * 1e-3) / 1e9
     traffic = None
     tpath = os.path.join(REPO, "profiles", f"traffic_{args.config}.json")
-    if os.path.exists(tpath) and world == 1 and args.scale == 1.0:
+    issue = None
+    if os.path.exists(tpath) and world == 1 and args.scale == 1.0 and not args.reorder:
         try:
-            traffic = json.load(open(tpath)).get("dram_bytes_per_launch")
+            tj = json.load(open(tpath))
+            traffic = tj.get("dram_bytes_per_launch")
+            if tj.get("warp_inst_per_launch"):
+                # the second roof (DESIGN 5b): warp-instructions per launch
+                # (ncu smsp__inst_executed.sum) at 4 issues/clk/SM on every SM
+                clk_mhz = 1965.0
+                sms = torch.cuda.get_device_properties(dev).multi_processor_count
+                t_issue = tj["warp_inst_per_launch"] / (sms * 4 * clk_mhz * 1e6) * 1e3
+                issue = {"warp_inst_per_launch": tj["warp_inst_per_launch"], "issue_bound_ms": t_issue,
+                         "frac": t_issue / ms_local, "sm_mhz": clk_mhz,
+                         "ncu_issue_active_pct": tj.get("issue_active_pct"), "source": tj.get("source")}
         except Exception:
             traffic = None
     comp = min(format_size_bytes(m, f, esz) for f in ("csr", "coo", "sell")) / size
@@ -586,6 +597,7 @@ def main():
                 "path": "dtans_spmv_host (C ABI, pinned host x/y/out)", "matches_device_result": ref_ok},
         "cusparse_csr": cus,
         "cusparse_formats": cus_fmt,
+        "issue_roofline": issue,
         "cpu_baseline": cpu,
         "clocks": clk.summary(),
         "gpu_launches": gpu_launches,
