@@ -271,6 +271,9 @@ class NcclComm:
         ro = np.ascontiguousarray(row_off, dtype=np.int64)
         if len(ro) != self.nranks + 1:
             raise ParameterError("row_off needs nranks + 1 entries")
+        want = torch.float64 if dev.precision == 8 else torch.float32
+        if x0.dtype != want or not x0.is_cuda or x0.numel() != int(ro[-1]):
+            raise ParameterError("x0 must be a full-length CUDA tensor in the container precision")
         x = x0.detach().clone().contiguous()
         lam = ctypes.c_double(float("nan"))
         st = torch.cuda.current_stream(x.device).cuda_stream if stream is None else stream
