@@ -155,7 +155,9 @@ TableBlock build_table_block(const uint8_t *recs, int precision)
     const char *er = getenv("DTANS_REP");
     const uint32_t rcap = er ? (uint32_t)std::max(1, atoi(er)) : 32u;
     tb.rep_v = (int32_t)pick_rep(tb.nv, vw, std::min<uint32_t>(rcap, 128u / vw), 36u * 1024u);
-    tb.rep_d = tb.dinline ? 1 : (int32_t)pick_rep(tb.nd, 4, std::min<uint32_t>(rcap, 32u), 8u * 1024u);
+    const char *edk = getenv("DTANS_DDICT_KB");  // shared-memory budget of the replicated delta dictionary
+    const uint32_t dbudget = (edk ? (uint32_t)std::max(1, atoi(edk)) : 8u) * 1024u;
+    tb.rep_d = tb.dinline ? 1 : (int32_t)pick_rep(tb.nd, 4, std::min<uint32_t>(rcap, 32u), dbudget);
     const size_t dict_d_bytes = tb.dinline ? 0 : align_up((size_t)(tb.nd + 1) * tb.rep_d * 4, 16);
     const size_t dict_v_bytes = align_up((size_t)(tb.nv + 1) * tb.rep_v * vw, 16);
     tb.tabs.assign(2 * kK, 0);
