@@ -102,7 +102,15 @@ int dtans_quantize(int64_t n, const uint64_t *symbols, const int64_t *counts,
                    int32_t *mult, int32_t *esc_mult, int32_t *esc_slots);
 
 /* ------------------------------------------------------------------ */
-/* Device container (sm_100a). */
+/* Device container (sm_100a).
+ *
+ * Threading (cf. spmv's `threads`, container.py:583-595): a handle is
+ * immutable after upload and its launches are ordered on the stream they are
+ * issued to.  Several streams may use one handle concurrently when the
+ * container has no long slices and no dynamic schedule (dtans_info: the
+ * plan); otherwise the per-handle scratch (partial sums of the long-slice
+ * tasks, the dynamic work counter) and the host-buffer path's staging are
+ * shared, so use one handle per stream or order the streams. */
 
 typedef struct dtans_dev dtans_dev; /* opaque */
 
