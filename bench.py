@@ -302,8 +302,17 @@ def run_powerit(args, world, rank, local):
     rows_of = [(cuts[r], cuts[r + 1]) for r in range(world)]
     t0 = time.time()
     m = synth.banded_rows(n, cuts[rank], cuts[rank + 1], 32, positive=True)
+    t_gen = time.time() - t0
+    t0 = time.time()
     c = P.encode_matrix(m)
     t_enc = time.time() - t0
+    enc_dev = {}
+    if not args.no_device_encode:
+        # the GPU encoder on the same 2^29-nnz shard: time and byte identity
+        t0 = time.time()
+        cd = P.encode_matrix(m, device=local)
+        enc_dev = {"encode_device_s": time.time() - t0, "encode_device_identical": bool(cd == c)}
+        del cd
     nnz_local = m.nnz
     del m
     op = D.ShardedSpMV.from_local(c, rows_of, rank, world, device=dev)
@@ -352,7 +361,7 @@ def run_powerit(args, world, rank, local):
                                       "iteration (dtans_mg_power_iteration, C ABI)" if args.driver == "capi" else
                                       "all_reduce(1 f64) + all_gather_into_tensor(y) per iteration (NCCL)"),
                       "driver": args.driver,
-                      "encode_s": t_enc},
+                      "generate_s": t_gen, "encode_s": t_enc, **enc_dev},
            "lambda": lam,
            "roofline": {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
                         "frac": achieved / pk["hbm_gbs"], "traffic": None, "peak_kind": pk_kind,
