@@ -214,11 +214,13 @@ def _host_vs_device(c, x, y, stages=None, monkeypatch=None):
     return out, ref
 
 
+@pytest.mark.parametrize("cta", ["0", "1"])
 @pytest.mark.parametrize("stages", [1, 8, 32])
 @pytest.mark.parametrize("gen", ["laplacian", "banded", "random"])
-def test_host_buffer_path_matches_device_path(gen, stages, monkeypatch):
-    """dtans_spmv_host (pipelined H2D / kernel / D2H, x sent per stage window
-    when the chunk windows are known) equals the device-pointer path bitwise."""
+def test_host_buffer_path_matches_device_path(gen, stages, cta, monkeypatch):
+    """dtans_spmv_host (pipelined H2D / kernel on chunk ranges / D2H) equals
+    the device-pointer path bitwise, with either main kernel."""
+    monkeypatch.setenv("DTANS_CTA", cta)
     m = {"laplacian": lambda: synth.laplacian_2d(700),
          "banded": lambda: synth.banded(200000, 27, levels=256, seed=4),
          "random": lambda: synth.config1_random(20000, 300000, seed=3)}[gen]()
