@@ -43,7 +43,7 @@ struct dtans_dev {
     size_t long_bytes = 0;
     int task_ctas = 0, task_smem = 0, solo_ctas = 0, solo_smem = 0;
     // CTA-pipelined main kernel (dtans_cta_kernel): ring of cta_stages buffers of cta_bufb bytes
-    bool cta_mode = false;
+    bool cta_mode = false, cta_fixed = false;
     int cta_stages = 0, cta_bufb = 0, cta_smem = 0;
     uint32_t *d_row_map = nullptr;  // optional output row map (reordered P*A)
     uint32_t *d_col_map = nullptr;  // optional column map (symmetric P*A*P^T): x'[j] = x[map[j]]
@@ -417,6 +417,7 @@ int launch(dtans_dev *h, const V *x, const V *y, V *out, const int64_t *row_star
         dev::KernelArgs b = a;
         b.bufb = h->cta_bufb;
         b.nstages = h->cta_stages;
+        b.cta_fixed = h->cta_fixed ? 1 : 0;
         const int cctas = (int)std::max<int64_t>(1, std::min<int64_t>(h->sms, nch));
         with_cta_kernel<V>(h->dinline, [&](auto kspmv, auto kspmv0, auto kdec, auto kscaled) -> int {
             if (scaled)
@@ -586,9 +587,30 @@ extern "C" int dtans_upload(const dtans_container_view *c, int device, dtans_dev
             // slices (one per consumer warp) in a CTA ring of >= 3 stages
             const char *ec = getenv("DTANS_CTA");
             const char *es = getenv("DTANS_CTA_STAGES");
-            const int64_t nst = es ? std::max(2, std::min(atoi(es), dev::kMaxCtaStages)) : 6;
+            int64_t nst = es ? std::max(2, std::min(atoi(es), dev::kMaxCtaStages)) : 6;
             const int64_t space = (int64_t)max_optin - sp.off_bufs - dev::kOverrunWords * 4;
-            const int64_t bb = space / nst / 16 * 16;  // stage bytes
+            int64_t bb = space / nst / 16 * 16;  // stage bytes
+            if (!es && ec && atoi(ec) != 0) {
+                // stages sized for full 31-slice chunks (consumer warp w <-> slice w)
+                // when at least 4 of them fit
+                uint64_t mxb = 0;
+                for (int64_t q = 0; q < nsl;) {
+                    if (is_long[q]) {
+                        q++;
+                        continue;
+                    }
+                    int64_t k = 1;
+                    while (k < dev::kCtaConsumers && q + k < nsl && !is_long[q + k]) k++;
+                    mxb = std::max(mxb, chunk_bytes(c->directory, q, k));
+                    q += k;
+                }
+                const int64_t fb = (int64_t)((mxb + 15) / 16 * 16);
+                if (fb > 0 && space / fb >= 4) {
+                    bb = fb;
+                    nst = std::min<int64_t>(dev::kMaxCtaStages, space / fb);
+                    h->cta_fixed = true;
+                }
+            }
             if (!dyn && ec && atoi(ec) != 0 && bb >= (int64_t)sp.bufb && bb / 4 < 65536) {
                 h->cta_mode = true;
                 h->cta_stages = (int)nst;

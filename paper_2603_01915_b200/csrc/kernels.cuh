@@ -145,6 +145,7 @@ struct KernelArgs {
     int32_t dynamic;              // 1: atomic ticket counter instead of a static stride
     uint32_t *work_counter;       // zeroed before every dynamic launch
     int32_t nstages;              // CTA-pipelined kernel: stage buffers of bufb bytes in the CTA ring
+    int32_t cta_fixed;            // stages sized for full chunks: consumer warp w <-> slice w
 };
 
 __device__ __forceinline__ uint32_t lanemask_lt()
@@ -983,6 +984,30 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) dtans_cta_kernel(const Kern
         }
         if (a.sumsq_zero != nullptr && blockIdx.x == 0 && threadIdx.x == 0) *a.sumsq_zero = 0.0;
     }
+    if (a.cta_fixed) {
+        // stages sized for full chunks: consumer w decodes slice w of each
+        for (uint32_t i = 0;; i++) {
+            const uint32_t slot = i % S;
+            mbar_wait(full + 8u * slot, (i / S) & 1u);
+            const uint2 md = ld_shared_v2(metas + 8u * slot);
+            const uint32_t k = md.y;
+            if (k == 0) break;  // uniform: the producer's end marker
+            if ((uint32_t)warp < k) {
+                const uint32_t w = (uint32_t)warp;
+                const uint32_t buf = bufs + slot * (uint32_t)a.bufb;
+                const uint32_t hw = chunk_hdr_words(k);
+                const uint32_t meta = sh32(buf + 4u * w);
+                const uint32_t dstart = w ? (sh32(buf + 4u * w - 4u) & 0xFFFFu) : 0u;
+                const uint32_t n = sh32(buf + (hw + w * 32u + (uint32_t)lane) * 4u);
+                const SmemSrc src{buf + (hw + k * 32u + dstart) * 4u};
+                decode_slice<V, kDecode, kHasY, kDIn, kScaled>(a, C, x, src, (meta & 0xFFFFu) - dstart, meta, n,
+                                                                (md.x + w) * kSliceRows + (uint32_t)lane, lane,
+                                                                scale, wsum);
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(empty + 8u * slot);
+        }
+    } else {
     // consumer w takes the CTA's slices w, w + kCtaConsumers, ... across the
     // stage sequence (stages hold k <= kCtaConsumers slices each) and
     // releases every stage once, when it moves past it
@@ -1010,6 +1035,7 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) dtans_cta_kernel(const Kern
         const SmemSrc src{buf + (hw + k * 32u + dstart) * 4u};
         decode_slice<V, kDecode, kHasY, kDIn, kScaled>(a, C, x, src, (meta & 0xFFFFu) - dstart, meta, n,
                                                         (md.x + w) * kSliceRows + (uint32_t)lane, lane, scale, wsum);
+    }
     }
     if (kScaled && a.sumsq_out != nullptr) {
 #pragma unroll
