@@ -6,6 +6,7 @@ import pytest
 
 import golden_cases as G
 from oracle import oracle as O
+import paper_2603_01915_b200 as P
 
 WITH_BYTES = [n for n in G.names() if "container" in G.load(n)]
 
@@ -50,3 +51,15 @@ def test_oracle_detects_consumption_mismatch():
     c.directory = d
     with pytest.raises(O.OracleError):
         O.decode(c)
+
+
+@pytest.mark.parametrize("name", [n for n in G.names() if "reference_spmv" in G.load(n)])
+def test_package_reference_spmv_bitwise(name):
+    """The package's reference_spmv (sparse.py:330-353 restated; D13) equals
+    the reference's own output bit for bit."""
+    rec = G.load(name)
+    m = G.matrix(rec)
+    if G.encode_kwargs(rec).get("value_width") == 4:  # the golden was made on the f32 matrix
+        m = P.CsrMatrix(m.rows, m.cols, m.row_start, m.col_idx, m.values.astype(np.float32))
+    out = P.reference_spmv(m, rec["x"], rec["y"])
+    assert G.same_bits_or_nan(out, rec["reference_spmv"])
