@@ -359,14 +359,27 @@ __device__ __forceinline__ void lookup_pair(const Ctx &C, uint32_t sod, uint32_t
 //   payload_probe: 0 = no escape in the warp, 1 = fast case (every lane needs
 //   at most one payload word: its rank among the escaping lanes; f64 value
 //   escapes never qualify), 2 = general case.
-template <typename T>
+template <typename T, int NP = 4>
 __device__ __forceinline__ int payload_probe(const Ctx &C, const bool act, const uint32_t e[8], bool &dany)
 {
     const uint32_t FULL = 0xFFFFFFFFu;
-    // cheap test first: escape entries are the largest entries of a table
-    const uint32_t m02 = max(e[0], e[2]), m46 = max(e[4], e[6]);
-    const uint32_t dmax = max(m02, m46);
-    const uint32_t vmax = max(max(e[1], e[3]), max(e[5], e[7]));
+    // cheap test first: escape entries are the largest entries of a table.
+    // NP < 4 (final segments): pairs past NP are pads of a table with a pad
+    // symbol, never escapes, and are not looked at.
+    uint32_t dmax, vmax;
+    if (NP == 4) {
+        dmax = max(max(e[0], e[2]), max(e[4], e[6]));
+        vmax = max(max(e[1], e[3]), max(e[5], e[7]));
+    } else if (NP == 3) {
+        dmax = max(max(e[0], e[2]), e[4]);
+        vmax = max(max(e[1], e[3]), e[5]);
+    } else if (NP == 2) {
+        dmax = max(e[0], e[2]);
+        vmax = max(e[1], e[3]);
+    } else {
+        dmax = e[0];
+        vmax = e[1];
+    }
     dany = act && dmax >= C.desc_min;
     const bool vany = act && vmax >= C.vesc_min;
     if (!__any_sync(FULL, dany || vany)) return 0;
@@ -374,16 +387,24 @@ __device__ __forceinline__ int payload_probe(const Ctx &C, const bool act, const
     if (T::kPayloadWords == 2) {
         // f64: no value escape, and at most one delta escape per lane, i.e.
         // the second-largest delta entry does not escape
-        const uint32_t d2 = max(max(min(e[0], e[2]), min(e[4], e[6])), min(m02, m46));
+        uint32_t d2 = 0u;
+        if (NP == 4) {
+            const uint32_t m02 = max(e[0], e[2]), m46 = max(e[4], e[6]);
+            d2 = max(max(min(e[0], e[2]), min(e[4], e[6])), min(m02, m46));
+        } else if (NP == 3) {
+            d2 = max(min(e[0], e[2]), min(max(e[0], e[2]), e[4]));
+        } else if (NP == 2) {
+            d2 = min(e[0], e[2]);
+        }
         fast = !vany && !(act && d2 >= C.desc_min);
     } else {
-        const bool d0 = e[0] >= C.desc_min, d1 = e[2] >= C.desc_min, d2 = e[4] >= C.desc_min,
-                   d3 = e[6] >= C.desc_min;
-        const bool dmulti = (d0 && (d1 || d2 || d3)) || (d1 && (d2 || d3)) || (d2 && d3);
-        const bool v0 = e[1] >= C.vesc_min, v1 = e[3] >= C.vesc_min, v2 = e[5] >= C.vesc_min,
-                   v3 = e[7] >= C.vesc_min;
-        const bool vmulti = (v0 && (v1 || v2 || v3)) || (v1 && (v2 || v3)) || (v2 && v3);
-        fast = !act || !(dmulti || vmulti || (dany && vany));
+        int nd = 0, nv = 0;
+#pragma unroll
+        for (int p = 0; p < NP; p++) {
+            nd += e[2 * p] >= C.desc_min ? 1 : 0;
+            nv += e[2 * p + 1] >= C.vesc_min ? 1 : 0;
+        }
+        fast = !act || nd + nv <= 1;
     }
     return __all_sync(FULL, fast) ? 1 : 2;
 }
@@ -391,7 +412,7 @@ __device__ __forceinline__ int payload_probe(const Ctx &C, const bool act, const
 // Fast payload event: every lane reads at most one word, at its rank among
 // the escaping lanes.  f64 (kPayloadWords == 2): only a delta can escape
 // here, so `dany` (from the probe) is the lane's escape flag.
-template <typename T, class Src>
+template <typename T, class Src, int NP = 4>
 __device__ __forceinline__ void payload_fast(const Ctx &C, const Src &src, uint32_t &cur, const bool act,
                                              const bool dany, const uint32_t e[8], uint32_t ds[4],
                                              typename T::Bits vs[4])
@@ -400,19 +421,19 @@ __device__ __forceinline__ void payload_fast(const Ctx &C, const Src &src, uint3
     bool esc = dany;
     if (T::kPayloadWords == 1) {
 #pragma unroll
-        for (int k = 1; k < 8; k += 2) esc = esc || (act && e[k] >= C.vesc_min);
+        for (int p = 0; p < NP; p++) esc = esc || (act && e[2 * p + 1] >= C.vesc_min);
     }
     const uint32_t m = __ballot_sync(0xFFFFFFFFu, esc);
     const uint32_t w = src(cur + __popc(m & C.lt));
     cur += __popc(m);
 #pragma unroll
-    for (int p = 0; p < 4; p++) {
+    for (int p = 0; p < NP; p++) {
         if (e[2 * p] >= C.desc_min) ds[p] = w;
         if (T::kPayloadWords == 1 && e[2 * p + 1] >= C.vesc_min) vs[p] = (Bits)w;
     }
 }
 
-template <typename T, class Src>
+template <typename T, class Src, int NP = 4>
 __device__ __forceinline__ void payload_slow(const Ctx &C, const Src &src, uint32_t &cur, const bool act,
                                              const uint32_t e[8], uint32_t ds[4], typename T::Bits vs[4])
 {
@@ -420,7 +441,7 @@ __device__ __forceinline__ void payload_slow(const Ctx &C, const Src &src, uint3
     const uint32_t FULL = 0xFFFFFFFFu;
     uint32_t pc = 0;
 #pragma unroll
-    for (int p = 0; p < 4; p++)
+    for (int p = 0; p < NP; p++)
         pc += (e[2 * p] >= C.desc_min ? 1u : 0u) + (e[2 * p + 1] >= C.vesc_min ? (uint32_t)T::kPayloadWords : 0u);
     if (!act) pc = 0;
     // exclusive warp scan of pc (<= 12 words: 4 bit planes), one ballot per
@@ -435,7 +456,7 @@ __device__ __forceinline__ void payload_slow(const Ctx &C, const Src &src, uint3
     if (pc) {
         uint32_t off = cur + excl;
 #pragma unroll
-        for (int p = 0; p < 4; p++) {
+        for (int p = 0; p < NP; p++) {
             if (e[2 * p] >= C.desc_min) {
                 ds[p] = src(off);
                 off += 1;
@@ -456,14 +477,14 @@ __device__ __forceinline__ void payload_slow(const Ctx &C, const Src &src, uint3
 
 // All three in one (final segments and the solo path, where the extra
 // copy is not worth it).
-template <typename T, class Src>
+template <typename T, class Src, int NP = 4>
 __device__ __forceinline__ void payload_event(const Ctx &C, const Src &src, uint32_t &cur, const bool act,
                                               const uint32_t e[8], uint32_t ds[4], typename T::Bits vs[4])
 {
     bool dany;
-    const int pk = payload_probe<T>(C, act, e, dany);
-    if (pk == 1) payload_fast<T>(C, src, cur, act, dany, e, ds, vs);
-    else if (pk == 2) payload_slow<T>(C, src, cur, act, e, ds, vs);
+    const int pk = payload_probe<T, NP>(C, act, e, dany);
+    if (pk == 1) payload_fast<T, Src, NP>(C, src, cur, act, dany, e, ds, vs);
+    else if (pk == 2) payload_slow<T, Src, NP>(C, src, cur, act, e, ds, vs);
 }
 
 __device__ __forceinline__ uint32_t byte1(uint32_t x) { return __byte_perm(x, 0u, 0x4441u); }
@@ -626,7 +647,8 @@ __device__ __forceinline__ void final_segment(const KernelArgs &a, const Ctx &C,
             vs[p] = 0;
         }
     }
-    payload_event<T>(C, src, st.cur, act, e, ds, vs);
+    // the event over the NP pairs only (pads past them never escape)
+    payload_event<T, Src, NP>(C, src, st.cur, act, e, ds, vs);
     const uint32_t base = 8u * jf;
 #pragma unroll
     for (int p = 0; p < NP; p++) {
