@@ -741,6 +741,40 @@ __device__ __forceinline__ void init_state(const Ctx &C, Src &src, const uint32_
     st.acc = V(0);
 }
 
+// y is read once and y' written once per SpMV: stream them past L2
+// (evict-first loads, .cs stores) so the gathered x stays resident.
+#ifndef DTANS_YSTREAM
+#define DTANS_YSTREAM 1
+#endif
+template <typename V> __device__ __forceinline__ V ld_stream(const V *p)
+{
+#if DTANS_YSTREAM
+    V v;
+    if (sizeof(V) == 8) {
+        unsigned long long b;
+        asm("{\n.reg .b64 pol;\ncreatepolicy.fractional.L2::evict_first.b64 pol, 1.0;\n"
+            "ld.global.nc.L1::no_allocate.L2::cache_hint.b64 %0, [%1], pol;\n}" : "=l"(b) : "l"(p));
+        memcpy(&v, &b, 8);
+    } else {
+        uint32_t b;
+        asm("{\n.reg .b64 pol;\ncreatepolicy.fractional.L2::evict_first.b64 pol, 1.0;\n"
+            "ld.global.nc.L1::no_allocate.L2::cache_hint.b32 %0, [%1], pol;\n}" : "=r"(b) : "l"(p));
+        memcpy(&v, &b, 4);
+    }
+    return v;
+#else
+    return __ldg(p);
+#endif
+}
+template <typename V> __device__ __forceinline__ void st_stream(V *p, V v)
+{
+#if DTANS_YSTREAM
+    __stcs(p, v);
+#else
+    *p = v;
+#endif
+}
+
 // consumption check (container.py:499-500) and column bound, one vote
 __device__ __forceinline__ void report(const KernelArgs &a, const Ctx &C, bool ok, uint32_t cur, uint32_t end,
                                        uint32_t n, uint32_t col, int lane)
@@ -769,7 +803,7 @@ __device__ __forceinline__ void decode_slice(const KernelArgs &a, const Ctx &C, 
     uint32_t orow = row;
     if (a.row_map != nullptr && inrow) orow = __ldg(a.row_map + row);
     V yv = V(0);
-    if (kHasY && inrow) yv = __ldg(reinterpret_cast<const V *>(a.y) + orow);
+    if (kHasY && inrow) yv = ld_stream(reinterpret_cast<const V *>(a.y) + orow);
     LaneState<V> st;
     st.out_pos = 0;
     if (kDecode && inrow) st.out_pos = __ldg(a.row_start + row);
@@ -784,7 +818,7 @@ __device__ __forceinline__ void decode_slice(const KernelArgs &a, const Ctx &C, 
             res = T::mul(res, scale);
             wsum = __dadd_rn(wsum, __dmul_rn((double)res, (double)res));
         }
-        reinterpret_cast<V *>(a.out)[orow] = res;
+        st_stream(reinterpret_cast<V *>(a.out) + orow, res);
     }
 }
 
