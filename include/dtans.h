@@ -152,7 +152,8 @@ int dtans_spmv_f32(dtans_dev *h, const float *x, const float *y, float *out,
  *   *sumsq_out += sum(out^2)              (f64 accumulation, atomic per warp)
  *   *sumsq_zero = 0                       (the next step's accumulator)
  * Device pointers; x and out in the container precision; the three scalars
- * must be distinct.  Containers with long slices are refused (PARAM). */
+ * must be distinct.  Long slices (checkpointed tasks) are scaled and summed
+ * in the task / finalize kernels, so any container is accepted. */
 int dtans_spmv_scaled(dtans_dev *h, const void *x, void *out, const double *sumsq_in,
                       double *sumsq_out, double *sumsq_zero, void *stream);
 
@@ -212,6 +213,19 @@ int dtans_set_col_map(dtans_dev *h, const uint32_t *host_map);
 
 /* Number of dtANS kernels launched by this handle so far (bench evidence). */
 int64_t dtans_launch_count(const dtans_dev *h);
+
+/* The work plan dtans_upload chose (no reference counterpart: tests use it
+ * to prove which kernel path a parity case ran, bench.py prints it). */
+typedef struct {
+    int64_t nchunks;          /* chunks of the main kernel */
+    int64_t chunk_slices_max; /* most slices in one chunk */
+    int64_t staged_slices;    /* slices the main kernel decodes (the rest are long) */
+    int64_t nlong, ntasks, nsolo; /* long slices and their checkpointed tasks */
+    int32_t dynamic;          /* atomic-ticket chunk claiming */
+    int32_t dinline;          /* delta symbols inline in the slot table */
+    int32_t bufb, nring;      /* staging buffer bytes, buffers per warp */
+} dtans_plan_t;
+int dtans_plan(const dtans_dev *h, dtans_plan_t *out);
 
 #ifdef __cplusplus
 }

@@ -26,6 +26,7 @@ EXPORTS = (
     "dtans_spmv_f32", "dtans_spmv_host", "dtans_decode", "dtans_check",
     "dtans_launch_count", "dtans_set_row_map", "dtans_spmv_scaled", "dtans_set_col_map",
     "dtans_encode_device", "dtans_mg_unique_id", "dtans_mg_init", "dtans_mg_free", "dtans_mg_power_iteration",
+    "dtans_plan",
 )
 
 
@@ -62,6 +63,16 @@ class ContainerView(ctypes.Structure):
         ("precision", ctypes.c_int32),
         ("tables", ctypes.c_void_p), ("row_symbols", ctypes.c_void_p),
         ("directory", ctypes.c_void_p), ("stream", ctypes.c_void_p),
+    ]
+
+
+class Plan(ctypes.Structure):
+    _fields_ = [
+        ("nchunks", ctypes.c_int64), ("chunk_slices_max", ctypes.c_int64),
+        ("staged_slices", ctypes.c_int64), ("nlong", ctypes.c_int64),
+        ("ntasks", ctypes.c_int64), ("nsolo", ctypes.c_int64),
+        ("dynamic", ctypes.c_int32), ("dinline", ctypes.c_int32),
+        ("bufb", ctypes.c_int32), ("nring", ctypes.c_int32),
     ]
 
 
@@ -105,6 +116,7 @@ def lib() -> ctypes.CDLL:
     L.dtans_set_col_map.argtypes = [vp, vp]
     L.dtans_launch_count.argtypes = [vp]
     L.dtans_launch_count.restype = i64
+    L.dtans_plan.argtypes = [vp, ctypes.POINTER(Plan)]
     _lib = L
     return L
 

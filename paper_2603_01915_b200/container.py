@@ -280,19 +280,32 @@ class DeviceContainer:
         return {"device_bytes": b.value, "ctas": ctas.value, "warps_per_cta": warps.value,
                 "smem_bytes": smem.value}
 
+    def plan(self) -> dict:
+        """The work plan of the upload (dtans_plan): chunks, long slices, ..."""
+        p = _native.Plan()
+        _native.check(_native.lib().dtans_plan(self.handle, ctypes.byref(p)))
+        return {k: getattr(p, k) for k, _ in _native.Plan._fields_}
+
     def launches(self) -> int:
         return int(_native.lib().dtans_launch_count(self.handle))
+
+    def _check_vec(self, t, n, what, dt):
+        if (t.dtype != dt or t.numel() != n or not t.is_cuda or not t.is_contiguous()
+                or t.device.index != self.device):
+            raise ParameterError(f"{what} must be a contiguous tensor on cuda:{self.device} "
+                                 f"of the container dtype with {n} elements")
 
     def spmv(self, x, y=None, out=None, stream=None):
         """y' = A x (+ y) on torch CUDA tensors; asynchronous."""
         torch = _torch()
         dt = torch.float64 if self.precision == 8 else torch.float32
-        if x.dtype != dt or x.numel() != self.cols or not x.is_cuda:
-            raise ParameterError("x must be a contiguous CUDA tensor of the container dtype/size")
-        if y is not None and (y.dtype != dt or y.numel() != self.rows or not y.is_cuda):
-            raise ParameterError("y must be a CUDA tensor of the container dtype/size")
+        self._check_vec(x, self.cols, "x", dt)
+        if y is not None:
+            self._check_vec(y, self.rows, "y", dt)
         if out is None:
             out = torch.empty(self.rows, dtype=dt, device=x.device)
+        else:
+            self._check_vec(out, self.rows, "out", dt)
         if stream is None:
             stream = torch.cuda.current_stream(x.device).cuda_stream
         fn = _native.lib().dtans_spmv_f64 if self.precision == 8 else _native.lib().dtans_spmv_f32
@@ -306,10 +319,11 @@ class DeviceContainer:
         sumsq_out += sum(out^2), sumsq_zero = 0 (f64 device scalars)."""
         torch = _torch()
         dt = torch.float64 if self.precision == 8 else torch.float32
-        if x.dtype != dt or x.numel() != self.cols or not x.is_cuda:
-            raise ParameterError("x must be a contiguous CUDA tensor of the container dtype/size")
-        if out.dtype != dt or out.numel() != self.rows or not out.is_cuda:
-            raise ParameterError("out must be a CUDA tensor of the container dtype/size")
+        self._check_vec(x, self.cols, "x", dt)
+        self._check_vec(out, self.rows, "out", dt)
+        for s in (sumsq_in, sumsq_out, sumsq_zero):
+            if s is not None and (s.dtype != torch.float64 or s.numel() < 1 or not s.is_cuda):
+                raise ParameterError("sum-of-squares scalars must be f64 CUDA tensors")
         if stream is None:
             stream = torch.cuda.current_stream(x.device).cuda_stream
         ptr = (lambda t: t.data_ptr() if t is not None else None)
@@ -326,6 +340,13 @@ class DeviceContainer:
 
     def spmv_host(self, x: np.ndarray, y: np.ndarray | None, out: np.ndarray) -> np.ndarray:
         """Host x, y, out (ideally pinned): H2D, kernel, D2H, check."""
+        dt = self.dtype
+        for a, n, what in ((x, self.cols, "x"), (y, self.rows, "y"), (out, self.rows, "out")):
+            if a is None and what == "y":
+                continue
+            if (not isinstance(a, np.ndarray) or a.dtype != dt or a.size != max(n, 1 if what == "x" else 0)
+                    or not a.flags.c_contiguous or (what == "out" and not a.flags.writeable)):
+                raise ParameterError(f"{what} must be a contiguous {np.dtype(dt).name} array of {n} elements")
         _native.check(_native.lib().dtans_spmv_host(
             self.handle, x.ctypes.data, y.ctypes.data if y is not None else None, out.ctypes.data))
         return out

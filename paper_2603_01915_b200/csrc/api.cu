@@ -445,6 +445,8 @@ int launch(dtans_dev *h, const V *x, const V *y, V *out, const int64_t *row_star
         });
         h->launches++;
     }
+    if (scaled && nch <= 0 && sumsq_zero != nullptr)  // the main kernel zeroes it otherwise
+        CK(cudaMemsetAsync(sumsq_zero, 0, sizeof(double), st), "zero sum of squares");
     if (a.nlong && c_lo < 0) {
         with_long_kernels<V>(h->dinline, [&](auto kt, auto ktd, auto ks, auto ksd) -> int {
             if (decode_only) {
@@ -809,8 +811,6 @@ extern "C" int dtans_set_row_map(dtans_dev *h, const uint32_t *host_map)
     CK(cudaSetDevice(h->device), "cudaSetDevice");
     if (!host_map) {
         if (h->d_row_map) cudaFree(h->d_row_map);
-    if (h->d_col_map) cudaFree(h->d_col_map);
-    if (h->d_xperm) cudaFree(h->d_xperm);
         h->d_row_map = nullptr;
         h->base.row_map = nullptr;
         return DTANS_OK;
@@ -854,6 +854,25 @@ extern "C" int dtans_set_col_map(dtans_dev *h, const uint32_t *host_map)
 
 extern "C" int64_t dtans_launch_count(const dtans_dev *h) { return h ? h->launches : 0; }
 
+extern "C" int dtans_plan(const dtans_dev *h, dtans_plan_t *out)
+{
+    if (!h || !out) return fail(DTANS_E_PARAM, "null argument");
+    *out = dtans_plan_t{};
+    out->nchunks = (int64_t)h->chunks.size();
+    for (const dev::ChunkRec &r : h->chunks) {
+        out->chunk_slices_max = std::max<int64_t>(out->chunk_slices_max, r.kw & 0xFF);
+        out->staged_slices += r.kw & 0xFF;
+    }
+    out->nlong = h->base.nlong;
+    out->ntasks = h->base.ntasks;
+    out->nsolo = h->base.nsolo;
+    out->dynamic = h->base.dynamic;
+    out->dinline = h->dinline ? 1 : 0;
+    out->bufb = h->base.bufb;
+    out->nring = h->base.nring;
+    return DTANS_OK;
+}
+
 extern "C" int dtans_spmv_f64(dtans_dev *h, const double *x, const double *y, double *out,
                               void *stream)
 {
@@ -876,7 +895,6 @@ extern "C" int dtans_spmv_scaled(dtans_dev *h, const void *x, void *out, const d
                                  double *sumsq_zero, void *stream)
 {
     if (!h) return fail(DTANS_E_PARAM, "null handle");
-    if (h->base.nlong) return fail(DTANS_E_PARAM, "the scaled SpMV needs a container without long slices");
     CK(cudaSetDevice(h->device), "cudaSetDevice");
     if (h->precision == 8)
         return launch<double>(h, (const double *)x, nullptr, (double *)out, nullptr, nullptr, nullptr, false,

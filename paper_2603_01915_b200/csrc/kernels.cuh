@@ -1121,6 +1121,10 @@ __global__ void __launch_bounds__(kTaskWarps * 32, 1024 / (kTaskWarps * 32)) dta
     const Ctx C = make_ctx<V>(a, lane);
     const V *__restrict__ x = reinterpret_cast<const V *>(a.x);
     const unsigned long long pol = policy_evict_first();
+    // power iteration (sumsq_out set): single-task slices are final here, so
+    // they are scaled and their squares summed like the main kernel's rows
+    const V scale = a.sumsq_in != nullptr ? (V)__ddiv_rn(1.0, __dsqrt_rn(*a.sumsq_in)) : V(1);
+    double wsum = 0.0;
     for (uint32_t t = blockIdx.x * warps + warp; t < a.ntasks; t += gridDim.x * warps) {
         const LongTask tk = a.tasks[t];
         const uint32_t row = tk.slice * kSliceRows + lane;
@@ -1167,12 +1171,21 @@ __global__ void __launch_bounds__(kTaskWarps * 32, 1024 / (kTaskWarps * 32)) dta
                     const uint32_t orow = a.row_map != nullptr ? __ldg(a.row_map + row) : row;
                     V res = st.acc;
                     if (a.y != nullptr) res = ValueTraits<V>::add(res, reinterpret_cast<const V *>(a.y)[orow]);
+                    if (a.sumsq_out != nullptr) {
+                        res = ValueTraits<V>::mul(res, scale);
+                        wsum = __dadd_rn(wsum, __dmul_rn((double)res, (double)res));
+                    }
                     reinterpret_cast<V *>(a.out)[orow] = res;
                 }
             } else {
                 reinterpret_cast<V *>(a.partials)[(size_t)tk.part * 32 + lane] = st.acc;
             }
         }
+    }
+    if (!kDecode && a.sumsq_out != nullptr) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) wsum = __dadd_rn(wsum, __shfl_xor_sync(0xFFFFFFFFu, wsum, o));
+        if (lane == 0 && wsum != 0.0) atomicAdd(a.sumsq_out, wsum);
     }
 }
 
@@ -1292,12 +1305,24 @@ __global__ void __launch_bounds__(256) dtans_finalize_kernel(const KernelArgs a)
     __shared__ V red[8][32];
     const uint32_t lane = threadIdx.x & 31u, w = threadIdx.x >> 5;
     const V *parts = reinterpret_cast<const V *>(a.partials);
+    // power iteration (sumsq_out set): scale, and sum the squares (one f64
+    // atomic per warp)
     auto finish = [&](const LongSlice &ls, V s) {
         const uint32_t row = ls.slice * kSliceRows + lane;
+        double sq = 0.0;
         if (row < (uint32_t)a.rows) {
             const uint32_t orow = a.row_map != nullptr ? __ldg(a.row_map + row) : row;
             if (kHasY) s = T::add(s, reinterpret_cast<const V *>(a.y)[orow]);
+            if (a.sumsq_out != nullptr) {
+                if (a.sumsq_in != nullptr) s = T::mul(s, (V)__ddiv_rn(1.0, __dsqrt_rn(*a.sumsq_in)));
+                sq = __dmul_rn((double)s, (double)s);
+            }
             reinterpret_cast<V *>(a.out)[orow] = s;
+        }
+        if (a.sumsq_out != nullptr) {
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) sq = __dadd_rn(sq, __shfl_xor_sync(0xFFFFFFFFu, sq, o));
+            if (lane == 0 && sq != 0.0) atomicAdd(a.sumsq_out, sq);
         }
     };
     if (blockIdx.x < a.nlong_small_blocks) {

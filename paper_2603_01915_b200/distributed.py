@@ -159,7 +159,14 @@ def power_iteration(op: ShardedSpMV, x0, iters: int, group=None, return_history:
     if len(x0) != op.cols or op.cols != op.global_rows:
         raise ParameterError("power iteration needs a square matrix and a full-length x0")
     if fused is None:
-        fused = op._dev is not None and op.local.rows > 0 and not return_history
+        fused = op._dev is not None and not return_history
+        if world > 1:
+            # every rank must take the same path (the two exchange different
+            # quantities); a rank with an injected spmv_fn cannot fuse
+            flag = torch.tensor([1 if fused else 0], dtype=torch.int32,
+                                device=x0.device if dist.get_backend(group) == "nccl" else "cpu")
+            dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=group)
+            fused = bool(flag.item())
     if fused:
         return _power_iteration_fused(op, x0, iters, group)
     x = x0.clone()
@@ -211,7 +218,10 @@ def _power_iteration_fused(op: ShardedSpMV, x0, iters: int, group=None):
     for k in range(iters):
         y = ybuf[k & 1]
         s_in = S[(k - 1) % 3: (k - 1) % 3 + 1] if k > 0 else None
-        op._dev.spmv_scaled(x, y[:rows], s_in, S[k % 3: k % 3 + 1], S[(k + 1) % 3: (k + 1) % 3 + 1])
+        if rows:
+            op._dev.spmv_scaled(x, y[:rows], s_in, S[k % 3: k % 3 + 1], S[(k + 1) % 3: (k + 1) % 3 + 1])
+        else:  # an empty shard adds nothing but still zeroes the next accumulator
+            S[(k + 1) % 3].zero_()
         if world > 1:
             dist.all_reduce(S[k % 3: k % 3 + 1], group=group)
             dist.all_gather_into_tensor(gathered, y, group=group)

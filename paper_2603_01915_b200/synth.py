@@ -39,17 +39,28 @@ def config1_random(n: int = 4096, nnz: int = 2**15, seed: int = 0) -> CsrMatrix:
 
 def laplacian_2d(g: int, dtype=np.float64) -> CsrMatrix:
     """Config 2: 5-point Laplacian on a g x g grid (diag 4, neighbours -1)."""
+    return laplacian_rows(g, 0, g * g, dtype)
+
+
+def laplacian_row_nnz(g: int) -> np.ndarray:
+    """Nonzeros per row of ``laplacian_2d(g)`` (shard planning without the matrix)."""
+    a, b = np.divmod(np.arange(g * g, dtype=np.int64), g)
+    return 1 + (a > 0) + (b > 0) + (b < g - 1) + (a < g - 1)
+
+
+def laplacian_rows(g: int, r0: int, r1: int, dtype=np.float64) -> CsrMatrix:
+    """Rows [r0, r1) of ``laplacian_2d(g)`` (a row shard; all columns)."""
     n = g * g
-    i = np.arange(n, dtype=np.int64)
+    i = np.arange(r0, r1, dtype=np.int64)
     a, b = np.divmod(i, g)
     offs = np.array([-g, -1, 0, 1, g], dtype=np.int64)
-    valid = np.stack([a > 0, b > 0, np.ones(n, bool), b < g - 1, a < g - 1], axis=1)
+    valid = np.stack([a > 0, b > 0, np.ones(len(i), bool), b < g - 1, a < g - 1], axis=1)
     cols = i[:, None] + offs[None, :]
     vals = np.where(offs == 0, 4.0, -1.0).astype(dtype)
-    vals = np.broadcast_to(vals, (n, 5))
-    row_start = np.zeros(n + 1, dtype=np.int64)
+    vals = np.broadcast_to(vals, (len(i), 5))
+    row_start = np.zeros(len(i) + 1, dtype=np.int64)
     np.cumsum(valid.sum(axis=1), out=row_start[1:])
-    return CsrMatrix(n, n, row_start, cols[valid], np.ascontiguousarray(vals[valid]))
+    return CsrMatrix(len(i), n, row_start, cols[valid], np.ascontiguousarray(vals[valid]))
 
 
 def banded(rows: int, band: int = 27, levels: int = 256, seed: int = 0,
@@ -81,6 +92,13 @@ def _splitmix64(z: np.ndarray) -> np.ndarray:
     z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
     z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
     return z ^ (z >> np.uint64(31))
+
+
+def banded_row_nnz(rows_total: int, band: int) -> np.ndarray:
+    """Nonzeros per row of the banded shape (shard planning without the matrix)."""
+    i = np.arange(rows_total, dtype=np.int64)
+    half = band // 2
+    return np.minimum(rows_total, i - half + band) - np.maximum(0, i - half)
 
 
 def banded_rows(rows_total: int, r0: int, r1: int, band: int = 32, levels: int = 256, seed: int = 0,

@@ -32,14 +32,15 @@ int fail(const char *what, int code)
 extern "C" const char *cmp_last_error(void) { return g_err; }
 
 // fmt: 0 = CSR ALG1, 1 = CSR ALG2, 2 = COO, 3 = SELL (slice 32).
-//   CSR:  a0 = row offsets (rows+1, int64), a1 = columns (nnz, int64), a2 = values
-//   COO:  a0 = row indices (nnz, int64),    a1 = columns,               a2 = values
-//   SELL: a0 = slice offsets (nslices+1, int64), a1 = columns (sell_size, int64, -1 = pad), a2 = values
-// prec 8 / 4.  Runs `warmup` then `iters` products on the legacy stream and
+//   CSR:  a0 = row offsets (rows+1), a1 = columns (nnz), a2 = values
+//   COO:  a0 = row indices (nnz),    a1 = columns,        a2 = values
+//   SELL: a0 = slice offsets (nslices+1), a1 = columns (sell_size, -1 = pad), a2 = values
+// Index arrays are int32 (ibits 32: the 4-byte indices of the CSR byte
+// model, reference sparse.py:185-198) or int64 (ibits 64).  prec 8 / 4.  Runs `warmup` then `iters` products on the legacy stream and
 // writes the mean milliseconds per product.
 extern "C" int cmp_spmv_time(int fmt, int64_t rows, int64_t cols, int64_t nnz, void *a0, void *a1, void *a2,
-                             int64_t sell_size, int prec, const void *x, void *y, int warmup, int iters,
-                             float *ms_out)
+                             int64_t sell_size, int prec, int ibits, const void *x, void *y, int warmup,
+                             int iters, float *ms_out)
 {
     int rc = 0;
     cusparseHandle_t h = nullptr;
@@ -54,21 +55,22 @@ extern "C" int cmp_spmv_time(int fmt, int64_t rows, int64_t cols, int64_t nnz, v
     cusparseSpMVAlg_t alg = CUSPARSE_SPMV_ALG_DEFAULT;
     size_t wb = 0;
     float ms = 0.f;
+    const cusparseIndexType_t it = ibits == 32 ? CUSPARSE_INDEX_32I : CUSPARSE_INDEX_64I;
     CSP(cusparseCreate(&h));
     switch (fmt) {
     case 0:
     case 1:
-        CSP(cusparseCreateCsr(&A, rows, cols, nnz, a0, a1, a2, CUSPARSE_INDEX_64I, CUSPARSE_INDEX_64I,
+        CSP(cusparseCreateCsr(&A, rows, cols, nnz, a0, a1, a2, it, it,
                               CUSPARSE_INDEX_BASE_ZERO, dt));
         alg = fmt == 0 ? CUSPARSE_SPMV_CSR_ALG1 : CUSPARSE_SPMV_CSR_ALG2;
         break;
     case 2:
-        CSP(cusparseCreateCoo(&A, rows, cols, nnz, a0, a1, a2, CUSPARSE_INDEX_64I, CUSPARSE_INDEX_BASE_ZERO, dt));
+        CSP(cusparseCreateCoo(&A, rows, cols, nnz, a0, a1, a2, it, CUSPARSE_INDEX_BASE_ZERO, dt));
         alg = CUSPARSE_SPMV_COO_ALG1;
         break;
     case 3:
-        CSP(cusparseCreateSlicedEll(&A, rows, cols, nnz, sell_size, 32, a0, a1, a2, CUSPARSE_INDEX_64I,
-                                    CUSPARSE_INDEX_64I, CUSPARSE_INDEX_BASE_ZERO, dt));
+        CSP(cusparseCreateSlicedEll(&A, rows, cols, nnz, sell_size, 32, a0, a1, a2, it, it,
+                                    CUSPARSE_INDEX_BASE_ZERO, dt));
         alg = CUSPARSE_SPMV_SELL_ALG1;
         break;
     default:
