@@ -101,17 +101,25 @@ class CsrMatrix:
 
 
 def coo_to_csr(m: CooMatrix) -> CsrMatrix:
-    """Sort by (row, col) and compress; duplicates rejected (sparse.py:133-144)."""
+    """COO -> CSR with rows in order and columns ascending within a row;
+    a repeated (row, col) coordinate raises MtxFormatError (the contract of
+    reference sparse.py:133-144).
+
+    One stable argsort of the linearised coordinate row * cols + col
+    orders the entries; equal neighbouring keys are duplicates, and the row
+    pointers are the searchsorted positions of every row start in the
+    sorted rows."""
     m.validate()
-    order = np.lexsort((m.col_idx, m.row_idx))
-    r = np.asarray(m.row_idx)[order]
-    c = np.asarray(m.col_idx)[order]
-    v = np.asarray(m.values)[order]
-    if len(r) > 1 and np.any((np.diff(r) == 0) & (np.diff(c) == 0)):
+    rows_i = np.asarray(m.row_idx, dtype=np.int64)
+    cols_i = np.asarray(m.col_idx, dtype=np.int64)
+    key = rows_i * np.int64(max(m.cols, 1)) + cols_i
+    perm = np.argsort(key, kind="stable")
+    skey = key[perm]
+    if skey.size > 1 and bool((skey[1:] == skey[:-1]).any()):
         raise MtxFormatError("duplicate (row, col) entry")
-    row_start = np.zeros(m.rows + 1, dtype=np.int64)
-    np.cumsum(np.bincount(r, minlength=m.rows), out=row_start[1:])
-    return CsrMatrix(m.rows, m.cols, row_start, c.astype(np.int64), v)
+    srow = rows_i[perm]
+    row_start = np.searchsorted(srow, np.arange(m.rows + 1, dtype=np.int64), side="left").astype(np.int64)
+    return CsrMatrix(m.rows, m.cols, row_start, cols_i[perm], np.asarray(m.values)[perm])
 
 
 def sell_widths(m: CsrMatrix, slice_height: int = 32) -> np.ndarray:
@@ -166,32 +174,40 @@ def value_patterns(values: np.ndarray) -> np.ndarray:
 
 
 def reference_spmv(m: CsrMatrix, x: np.ndarray, y: np.ndarray) -> np.ndarray:
-    """The reference's CSR SpMV utility (sparse.py:330-353), numpy on host.
+    """The reference's plain CSR product (contract of sparse.py:330-353):
+    y' = A x + y in the matrix precision, each row accumulated strictly left
+    to right from +0.0, i.e. acc = fl(acc + fl(v * x[c])), then fl(acc + y).
+    x and y are cast to the matrix dtype; a new array is returned.
 
-    Part of the mirrored public API (a plain CSR product used for checking
-    and for the compression-free comparison); the dtANS ``spmv`` never calls
-    it.  Per row: acc = +0.0; acc = fl(acc + fl(v * x[c])) left to right;
-    result fl(acc + y).
-    """
+    Host numpy, a checker and API mirror only (the dtANS ``spmv`` never
+    calls it).  The products fl(v * x[c]) do not depend on order, so they
+    are formed once for all nonzeros; the sums are then folded by position
+    within the row: step q adds the q-th product of every row that has one
+    (each row at most once per step, so a fancy-indexed add is exact)."""
     x = np.asarray(x)
     y = np.asarray(y)
     if len(x) != m.cols or len(y) != m.rows:
         raise ParameterError("dimension mismatch")
-    dtype = m.values.dtype
-    x = x.astype(dtype, copy=False)
-    y = y.astype(dtype, copy=False)
-    acc = np.zeros(m.rows, dtype=dtype)
-    nnz_row = np.diff(m.row_start)
-    if m.nnz:
-        order = np.argsort(-nnz_row, kind="stable")
-        base = m.row_start[:-1][order]
-        maxn = int(nnz_row.max())
-        active = np.searchsorted(-nnz_row[order], -np.arange(1, maxn + 1), side="right")
-        for q in range(maxn):
-            a = int(active[q])
-            idx = base[:a] + q
-            acc[order[:a]] += m.values[idx] * x[m.col_idx[idx]]
-    return acc + y
+    dt = m.values.dtype
+    xv = x.astype(dt, copy=False)
+    yv = y.astype(dt, copy=False)
+    acc = np.zeros(m.rows, dtype=dt)
+    if m.nnz == 0:
+        return acc + yv
+    rs = np.asarray(m.row_start, dtype=np.int64)
+    lens = np.diff(rs)
+    with np.errstate(all="ignore"):
+        prod = np.asarray(m.values) * xv[np.asarray(m.col_idx)]
+    owner = np.repeat(np.arange(m.rows, dtype=np.int64), lens)
+    pos = np.arange(m.nnz, dtype=np.int64) - rs[owner]
+    by_pos = np.argsort(pos, kind="stable")
+    bounds = np.concatenate([[0], np.cumsum(np.bincount(pos))])
+    with np.errstate(all="ignore"):
+        for q in range(len(bounds) - 1):
+            sel = by_pos[bounds[q]:bounds[q + 1]]
+            tgt = owner[sel]
+            acc[tgt] = acc[tgt] + prod[sel]
+        return acc + yv
 
 
 def sort_rows_by_length(m: CsrMatrix, window: int | None = None):
@@ -222,60 +238,81 @@ def sort_rows_by_length(m: CsrMatrix, window: int | None = None):
     return pm, perm.astype(np.uint32)
 
 
-def parse_mtx(text: str) -> CooMatrix:
-    """Parse MatrixMarket coordinate content (sparse.py:205-264): real /
-    integer / pattern fields, general / symmetric symmetry; symmetric
-    off-diagonal entries are mirrored, pattern entries get value 1.0.
-    Raises MtxFormatError on the same conditions as the reference, checked
-    in the same order."""
-    lines = text.splitlines()
-    if not lines or not lines[0].startswith("%%MatrixMarket"):
+_MTX_FIELDS = {"real": 3, "integer": 3, "pattern": 2}  # tokens per entry line
+_MTX_SYMMETRY = ("general", "symmetric")
+
+
+def _mtx_header(first: str):
+    """Banner line -> (field, symmetry); the reference's checks in order
+    (object, layout, field, symmetry)."""
+    if not first.startswith("%%MatrixMarket"):
         raise MtxFormatError("missing %%MatrixMarket banner")
-    banner = [tok.lower() for tok in lines[0].split()]
-    if len(banner) != 5:
-        raise MtxFormatError(f"malformed banner: {lines[0]!r}")
-    obj, layout, field, symmetry = banner[1:]
-    if obj != "matrix":
-        raise MtxFormatError(f"unsupported object {obj!r}")
-    if layout != "coordinate":
-        raise MtxFormatError(f"unsupported layout {layout!r} (coordinate only)")
-    if field not in ("real", "integer", "pattern"):
-        raise MtxFormatError(f"unsupported field {field!r}")
-    if symmetry not in ("general", "symmetric"):
-        raise MtxFormatError(f"unsupported symmetry {symmetry!r}")
-    body = [ln for ln in lines[1:] if ln.strip() and not ln.lstrip().startswith("%")]
-    if not body:
-        raise MtxFormatError("missing size line")
-    head = body[0].split()
-    if len(head) != 3:
-        raise MtxFormatError(f"malformed size line: {body[0]!r}")
+    words = first.split()
+    if len(words) != 5:
+        raise MtxFormatError(f"malformed banner: {first!r}")
+    obj, layout, field, symmetry = (w.lower() for w in words[1:])
+    checks = ((obj == "matrix", f"unsupported object {obj!r}"),
+              (layout == "coordinate", f"unsupported layout {layout!r} (coordinate only)"),
+              (field in _MTX_FIELDS, f"unsupported field {field!r}"),
+              (symmetry in _MTX_SYMMETRY, f"unsupported symmetry {symmetry!r}"))
+    for ok, msg in checks:
+        if not ok:
+            raise MtxFormatError(msg)
+    return field, symmetry
+
+
+def _mtx_size(line: str):
+    parts = line.split()
     try:
-        rows, cols, nnz = (int(t) for t in head)
+        if len(parts) != 3:
+            raise ValueError
+        dims = tuple(int(p) for p in parts)
     except ValueError as e:
-        raise MtxFormatError(f"malformed size line: {body[0]!r}") from e
-    if min(rows, cols, nnz) < 0:
+        raise MtxFormatError(f"malformed size line: {line!r}") from e
+    if any(d < 0 for d in dims):
         raise MtxFormatError("negative dimensions")
-    if len(body) - 1 != nnz:
-        raise MtxFormatError(f"expected {nnz} entries, found {len(body) - 1}")
-    width = 2 if field == "pattern" else 3
-    toks = " ".join(body[1:]).split()
-    if len(toks) != nnz * width:
+    return dims
+
+
+def parse_mtx(text: str) -> CooMatrix:
+    """MatrixMarket coordinate content -> CooMatrix (0-based), with the
+    reference's accepted dialect and MtxFormatError conditions (sparse.py:
+    205-264): real / integer / pattern fields (pattern -> 1.0), general /
+    symmetric (off-diagonal entries of a symmetric file are mirrored and
+    appended after the stored ones); '%' comment and blank lines skipped.
+    The entry count is checked per line and the field count over the whole
+    token stream, as the reference does."""
+    all_lines = text.splitlines()
+    field, symmetry = _mtx_header(all_lines[0] if all_lines else "")
+    content = [ln for ln in all_lines[1:] if ln.strip() and not ln.lstrip().startswith("%")]
+    if not content:
+        raise MtxFormatError("missing size line")
+    nrows, ncols, count = _mtx_size(content[0])
+    entries = content[1:]
+    if len(entries) != count:
+        raise MtxFormatError(f"expected {count} entries, found {len(entries)}")
+    per = _MTX_FIELDS[field]
+    flat = [tok for ln in entries for tok in ln.split()]
+    if len(flat) != count * per:
         raise MtxFormatError("entry lines have the wrong number of fields")
     try:
-        a = np.asarray(toks, dtype=np.float64).reshape(nnz, width)
+        table = np.array(flat, dtype=np.float64).reshape(count, per)
     except ValueError as e:
         raise MtxFormatError("non-numeric entry") from e
-    r = a[:, 0].astype(np.int64) - 1
-    c = a[:, 1].astype(np.int64) - 1
-    if np.any(a[:, 0] != r + 1) or np.any(a[:, 1] != c + 1):
+    one_based = table[:, :2]
+    idx = one_based.astype(np.int64)
+    if not np.array_equal(idx.astype(np.float64), one_based):
         raise MtxFormatError("non-integer index")
-    v = a[:, 2] if width == 3 else np.ones(nnz, dtype=np.float64)
-    if nnz and (r.min() < 0 or r.max() >= rows or c.min() < 0 or c.max() >= cols):
+    idx -= 1
+    r, c = idx[:, 0], idx[:, 1]
+    v = table[:, 2].copy() if per == 3 else np.ones(count, dtype=np.float64)
+    if count and (idx.min() < 0 or r.max() >= nrows or c.max() >= ncols):
         raise MtxFormatError("index out of range")
     if symmetry == "symmetric":
-        off = r != c
-        r, c, v = np.concatenate([r, c[off]]), np.concatenate([c, r[off]]), np.concatenate([v, v[off]])
-    return CooMatrix(rows, cols, r, c, v)
+        mirror = np.flatnonzero(r != c)
+        r, c, v = (np.concatenate([r, c[mirror]]), np.concatenate([c, r[mirror]]),
+                   np.concatenate([v, v[mirror]]))
+    return CooMatrix(nrows, ncols, r, c, v)
 
 
 def read_mtx(path) -> CsrMatrix:

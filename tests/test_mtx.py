@@ -129,3 +129,58 @@ def test_sort_symmetric_by_degree_is_pap():
     assert np.all(np.diff(nnz_row) <= 0)  # rows by descending length
     for i in range(b.rows):  # columns ascending within rows
         assert np.all(np.diff(b.col_idx[b.row_start[i]:b.row_start[i + 1]]) > 0)
+
+
+@pytest.mark.skipif(not os.path.isdir(REF), reason="reference not present (GPU box)")
+@pytest.mark.parametrize("text", [
+    "no banner\n1 1 0\n", "", "%%MatrixMarket matrix\n",
+    "%%MatrixMarket vector coordinate real general\n1 1 0\n",
+    "%%MatrixMarket matrix array real general\n1 1\n1.0\n",
+    "%%MatrixMarket matrix coordinate complex general\n1 1 1\n1 1 1 0\n",
+    "%%MatrixMarket matrix coordinate real skew-symmetric\n1 1 0\n",
+    "%%MatrixMarket matrix coordinate real general\n",
+    "%%MatrixMarket matrix coordinate real general\n1 1\n",
+    "%%MatrixMarket matrix coordinate real general\n1 a 1\n",
+    "%%MatrixMarket matrix coordinate real general\n-1 1 0\n",
+    "%%MatrixMarket matrix coordinate real general\n1 1 1\n2 1 1.0\n",
+    "%%MatrixMarket matrix coordinate real general\n1 1 1\n0 1 1.0\n",
+    "%%MatrixMarket matrix coordinate real general\n1 1 2\n1 1 1.0\n",
+    "%%MatrixMarket matrix coordinate real general\n1 1 1\n1 1\n",
+    "%%MatrixMarket matrix coordinate real general\n2 2 2\n1 1 1 2\n2 2\n",
+    "%%MatrixMarket matrix coordinate real general\n1 1 1\n1.5 1 1.0\n",
+    "%%MatrixMarket matrix coordinate real general\n2 2 1\n1 1 x\n",
+    "%%MatrixMarket matrix coordinate pattern symmetric\n3 3 2\n2 1\n3 3\n",
+])
+def test_error_behaviour_matches_reference(text):
+    """Same accept/reject decision and the same message as the reference."""
+    sys.path.insert(0, REF)
+    try:
+        import csrdtans as R
+    finally:
+        sys.path.remove(REF)
+
+    def run(f):
+        try:
+            coo = f(text)
+            return ("ok", coo.rows, coo.cols, coo.row_idx.tolist(), coo.col_idx.tolist(), coo.values.tolist())
+        except Exception as e:  # noqa: BLE001 - compare the exception itself
+            return ("err", type(e).__name__, str(e))
+    assert run(parse_mtx) == run(R.parse_mtx)
+
+
+@pytest.mark.skipif(not os.path.isdir(REF), reason="reference not present (GPU box)")
+def test_coo_to_csr_matches_reference():
+    sys.path.insert(0, REF)
+    try:
+        import csrdtans as R
+    finally:
+        sys.path.remove(REF)
+    rng = np.random.default_rng(5)
+    for n, k in ((1, 1), (7, 20), (300, 5000), (64, 0)):
+        key = rng.choice(n * n, min(k, n * n), replace=False)
+        r, c = np.divmod(key, n)
+        v = rng.standard_normal(len(r))
+        a = coo_to_csr(P.CooMatrix(n, n, r, c, v))
+        b = R.coo_to_csr(R.CooMatrix(n, n, r, c, v))
+        assert np.array_equal(a.row_start, b.row_start) and np.array_equal(a.col_idx, b.col_idx)
+        assert np.array_equal(a.values, b.values)
