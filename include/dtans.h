@@ -125,8 +125,14 @@ typedef struct {
     const uint32_t *stream;      /* nwords */
 } dtans_container_view;
 
-/* Upload + re-layout for the kernel (split per-domain slot tables, a
- * 16-byte padded stream, per-tile plans).  Synchronous. */
+/* Upload + re-layout for the kernel (replaces the reference's in-memory
+ * container + its lazily built decode arrays, container.py:344-367): the
+ * shared-memory table image, and the chunk blobs (slice metadata,
+ * row_symbols, stream words per chunk of slices) streamed to the device
+ * through two pinned staging buffers while worker threads assemble the next
+ * batch straight from the view's arrays -- which may point into an mmapped
+ * CDTA file (container.py:647-720, paper_2603_01915_b200.load).  No full
+ * host copy of the container is made.  Synchronous on return. */
 int dtans_upload(const dtans_container_view *c, int device, dtans_dev **out);
 void dtans_free(dtans_dev *h);
 
@@ -224,6 +230,8 @@ typedef struct {
     int32_t dynamic;          /* atomic-ticket chunk claiming */
     int32_t dinline;          /* delta symbols inline in the slot table */
     int32_t bufb, nring;      /* staging buffer bytes, buffers per warp */
+    int64_t upload_bytes;     /* bytes streamed through the pinned upload buffers */
+    int64_t upload_batches;   /* cudaMemcpyAsync batches of the upload */
 } dtans_plan_t;
 int dtans_plan(const dtans_dev *h, dtans_plan_t *out);
 

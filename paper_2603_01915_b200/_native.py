@@ -73,6 +73,7 @@ class Plan(ctypes.Structure):
         ("ntasks", ctypes.c_int64), ("nsolo", ctypes.c_int64),
         ("dynamic", ctypes.c_int32), ("dinline", ctypes.c_int32),
         ("bufb", ctypes.c_int32), ("nring", ctypes.c_int32),
+        ("upload_bytes", ctypes.c_int64), ("upload_batches", ctypes.c_int64),
     ]
 
 

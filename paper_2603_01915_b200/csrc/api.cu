@@ -38,13 +38,12 @@ struct dtans_dev {
     int ctas = 0, threads = 1024, smem = 0;
     int64_t launches = 0;
     int64_t staged_slices = 0;  // slices whose stream fits a ring buffer
+    size_t upload_staged_bytes = 0;  // bytes streamed through the pinned upload buffers
+    int64_t upload_batches = 0;
     // long-slice checkpoint index
     void *d_long = nullptr;     // tasks + pool + slices + partials
     size_t long_bytes = 0;
     int task_ctas = 0, task_smem = 0, solo_ctas = 0, solo_smem = 0;
-    // CTA-pipelined main kernel (dtans_cta_kernel): ring of cta_stages buffers of cta_bufb bytes
-    bool cta_mode = false, cta_fixed = false;
-    int cta_stages = 0, cta_bufb = 0, cta_smem = 0;
     uint32_t *d_row_map = nullptr;  // optional output row map (reordered P*A)
     uint32_t *d_col_map = nullptr;  // optional column map (symmetric P*A*P^T): x'[j] = x[map[j]]
     void *d_xperm = nullptr;        // x' scratch (cols values)
@@ -268,16 +267,6 @@ int with_kernel(bool dinline, F &&f)
 }
 
 template <typename V, class F>
-int with_cta_kernel(bool dinline, F &&f)
-{
-    if (dinline)
-        return f(dev::dtans_cta_kernel<V, false, true, true>, dev::dtans_cta_kernel<V, false, false, true>,
-                 dev::dtans_cta_kernel<V, true, false, true>, dev::dtans_cta_kernel<V, false, false, true, true>);
-    return f(dev::dtans_cta_kernel<V, false, true, false>, dev::dtans_cta_kernel<V, false, false, false>,
-             dev::dtans_cta_kernel<V, true, false, false>, dev::dtans_cta_kernel<V, false, false, false, true>);
-}
-
-template <typename V, class F>
 int with_long_kernels(bool dinline, F &&f)
 {
     if (dinline)
@@ -358,17 +347,6 @@ int configure(dtans_dev *h, const TableBlock &tb, const SmemPlan &sp)
     });
     if (rc) return rc;
     if (per_sm < 1) return fail(DTANS_E_CUDA, "kernel does not fit on an SM");
-    if (h->cta_mode) {
-        a.nstages = h->cta_stages;
-        rc = with_cta_kernel<V>(tb.dinline, [&](auto k0, auto k1, auto k2, auto k3) -> int {
-            CK(cudaFuncSetAttribute(k0, cudaFuncAttributeMaxDynamicSharedMemorySize, h->cta_smem), "attr");
-            CK(cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, h->cta_smem), "attr");
-            CK(cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, h->cta_smem), "attr");
-            CK(cudaFuncSetAttribute(k3, cudaFuncAttributeMaxDynamicSharedMemorySize, h->cta_smem), "attr");
-            return DTANS_OK;
-        });
-        if (rc) return rc;
-    }
     return DTANS_OK;
 }
 
@@ -413,25 +391,7 @@ int launch(dtans_dev *h, const V *x, const V *y, V *out, const int64_t *row_star
     a.sumsq_in = sumsq_in;
     a.sumsq_out = sumsq_out;
     a.sumsq_zero = sumsq_zero;
-    if (nch > 0 && h->cta_mode) {
-        dev::KernelArgs b = a;
-        b.bufb = h->cta_bufb;
-        b.nstages = h->cta_stages;
-        b.cta_fixed = h->cta_fixed ? 1 : 0;
-        const int cctas = (int)std::max<int64_t>(1, std::min<int64_t>(h->sms, nch));
-        with_cta_kernel<V>(h->dinline, [&](auto kspmv, auto kspmv0, auto kdec, auto kscaled) -> int {
-            if (scaled)
-                kscaled<<<cctas, h->threads, h->cta_smem, st>>>(b);
-            else if (decode_only)
-                kdec<<<cctas, h->threads, h->cta_smem, st>>>(b);
-            else if (y != nullptr)
-                kspmv<<<cctas, h->threads, h->cta_smem, st>>>(b);
-            else
-                kspmv0<<<cctas, h->threads, h->cta_smem, st>>>(b);
-            return 0;
-        });
-        h->launches++;
-    } else if (nch > 0) {
+    if (nch > 0) {
         with_kernel<V>(h->dinline, [&](auto kspmv, auto kspmv0, auto kdec, auto kscaled) -> int {
             if (scaled)
                 kscaled<<<ctas, h->threads, h->smem, st>>>(a);
@@ -471,6 +431,129 @@ int launch(dtans_dev *h, const V *x, const V *y, V *out, const int64_t *row_star
     CK(cudaGetLastError(), "kernel launch");
     return DTANS_OK;
 }
+
+// Worker threads over [0, n) in contiguous ranges (host-side assembly).
+template <class F>
+void parallel_for(size_t n, F &&f)
+{
+    const size_t nt = std::max<size_t>(1, std::min<size_t>({16, std::thread::hardware_concurrency(), (n + 63) / 64}));
+    if (nt <= 1) {
+        f(0, n);
+        return;
+    }
+    std::vector<std::thread> th;
+    for (size_t t = 0; t < nt; t++) th.emplace_back([&, t]() { f(n * t / nt, n * (t + 1) / nt); });
+    for (auto &t : th) t.join();
+}
+
+// One chunk blob (kernels.cuh ChunkRec): slice metadata words, the slices'
+// row_symbols, their stream words -- copied from the container arrays.
+void assemble_chunk(const dtans_container_view *c, const dev::ChunkRec &r, bool pads_ok, uint32_t *p)
+{
+    const int64_t s0 = r.s0, k = r.kw & 0xFF;
+    const uint64_t base = c->directory[s0];
+    for (int64_t i = 0; i < k; i++) {
+        // slice metadata word (kernels.cuh slice_meta)
+        const int64_t sr0 = (s0 + i) * kSlice;
+        uint32_t maxn = 0, minseg = 0xFFFFFFFFu;
+        for (int64_t l = 0; l < kSlice; l++) {
+            const uint32_t n = sr0 + l < c->rows ? c->row_symbols[sr0 + l] : 0u;
+            maxn = std::max(maxn, n);
+            minseg = std::min(minseg, (n + 7u) / 8u);
+        }
+        const uint32_t mseg = (maxn + 7u) / 8u;
+        const uint32_t np = pads_ok && mseg > 0 ? (maxn - 8u * (mseg - 1u)) / 2u : 4u;
+        p[i] = dev::slice_meta((uint32_t)(c->directory[s0 + i + 1] - base), mseg, minseg, np);
+    }
+    const uint32_t hw = dev::chunk_hdr_words((uint32_t)k);
+    for (uint32_t i = (uint32_t)k; i < hw; i++) p[i] = 0u;
+    p += hw;
+    const int64_t r0 = s0 * kSlice, r1 = std::min<int64_t>((s0 + k) * kSlice, c->rows);
+    memcpy(p, c->row_symbols + r0, sizeof(uint32_t) * (size_t)(r1 - r0));
+    for (int64_t i = r1 - r0; i < k * 32; i++) p[i] = 0u;
+    p += k * 32;
+    const uint64_t nw = c->directory[s0 + k] - base;
+    memcpy(p, c->stream + base, sizeof(uint32_t) * (size_t)nw);
+    for (uint64_t i = nw; i < ((nw + 3) & ~3ull); i++) p[i] = 0u;
+}
+
+// Host->device copies through two pinned staging buffers on one stream:
+// the host fills buffer b while buffer b^1's cudaMemcpyAsync is in flight.
+struct PinnedUploader {
+    static constexpr size_t kCap = (size_t)32 << 20;
+    size_t cap = kCap;
+    void *buf[2] = {nullptr, nullptr};
+    cudaEvent_t ev[2] = {nullptr, nullptr};
+    bool busy[2] = {false, false};
+    int cur = 0;
+    cudaStream_t st = nullptr;
+    cudaError_t err = cudaSuccess;
+    size_t bytes = 0;
+    int64_t batches = 0;
+
+    int init(int /*device*/)
+    {
+        // DTANS_UPLOAD_KB: staging buffer size (tests force many batches)
+        if (const char *e = getenv("DTANS_UPLOAD_KB")) cap = std::max<size_t>(64, (size_t)atoll(e)) << 10;
+        for (int b = 0; b < 2; b++) {
+            if ((err = cudaHostAlloc(&buf[b], cap, cudaHostAllocDefault)) != cudaSuccess) return cuda_fail(err, "cudaHostAlloc");
+            if ((err = cudaEventCreateWithFlags(&ev[b], cudaEventDisableTiming)) != cudaSuccess) return cuda_fail(err, "event");
+        }
+        if ((err = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking)) != cudaSuccess) return cuda_fail(err, "stream");
+        return DTANS_OK;
+    }
+    // the next free staging buffer (waits for its previous copy)
+    void *acquire()
+    {
+        if (busy[cur]) {
+            if ((err = cudaEventSynchronize(ev[cur])) != cudaSuccess) return nullptr;
+            busy[cur] = false;
+        }
+        return buf[cur];
+    }
+    bool submit(void *dst, size_t n)
+    {
+        if ((err = cudaMemcpyAsync(dst, buf[cur], n, cudaMemcpyHostToDevice, st)) != cudaSuccess) return false;
+        if ((err = cudaEventRecord(ev[cur], st)) != cudaSuccess) return false;
+        busy[cur] = true;
+        cur ^= 1;
+        bytes += n;
+        batches++;
+        return true;
+    }
+    // a plain array (pageable or mmapped) through the staging buffers
+    bool copy(void *dst, const void *src, size_t n)
+    {
+        const char *s = (const char *)src;
+        char *d = (char *)dst;
+        for (size_t o = 0; o < n; o += cap) {
+            const size_t len = std::min(cap, n - o);
+            char *b = (char *)acquire();
+            if (!b) return false;
+            parallel_for((len + 4095) / 4096, [&](size_t lo, size_t hi) {
+                memcpy(b + lo * 4096, s + o + lo * 4096, std::min(len, hi * 4096) - lo * 4096);
+            });
+            if (!submit(d + o, len)) return false;
+        }
+        return true;
+    }
+    bool finish()
+    {
+        if (st && (err = cudaStreamSynchronize(st)) != cudaSuccess) return false;
+        return true;
+    }
+    ~PinnedUploader()
+    {
+        if (st) {
+            cudaStreamSynchronize(st);
+            cudaStreamDestroy(st);
+        }
+        for (int b = 0; b < 2; b++) {
+            if (ev[b]) cudaEventDestroy(ev[b]);
+            if (buf[b]) cudaFreeHost(buf[b]);
+        }
+    }
+};
 
 }  // namespace
 
@@ -522,12 +605,11 @@ extern "C" int dtans_upload(const dtans_container_view *c, int device, dtans_dev
     }
     // staging ring: 2 buffers per warp (measured: larger chunks beat a
     // deeper ring; 32 warps x 2 chunks in flight cover the HBM latency)
-    const char *er = getenv("DTANS_RING");
     // DTANS_SMEM_KB caps the main kernel's shared memory (the rest of the
     // SM's 256 KB L1/shared array becomes L1 cache for the x gathers)
     const char *ek = getenv("DTANS_SMEM_KB");
     const int smem_cap = ek ? std::min(max_optin, atoi(ek) * 1024) : max_optin;
-    SmemPlan sp = plan_smem(tb, smem_cap, er ? std::max(1, std::min(3, atoi(er))) : 2);
+    SmemPlan sp = plan_smem(tb, smem_cap, dev::kMaxRing);
     if (sp.bufb < 512) {
         delete h;
         return fail(DTANS_E_CUDA, "coding tables leave no shared memory for staging");
@@ -585,40 +667,6 @@ extern "C" int dtans_upload(const dtans_container_view *c, int device, dtans_dev
             std::stable_sort(order.begin(), order.end(), [&](uint32_t p, uint32_t q) { return cost[p] > cost[q]; });
             for (uint32_t s : order) push(s, 1);
         } else {
-            // CTA-pipelined kernel (DTANS_CTA=1): chunks of up to kCtaConsumers
-            // slices (one per consumer warp) in a CTA ring of >= 3 stages
-            const char *ec = getenv("DTANS_CTA");
-            const char *es = getenv("DTANS_CTA_STAGES");
-            int64_t nst = es ? std::max(2, std::min(atoi(es), dev::kMaxCtaStages)) : 6;
-            const int64_t space = (int64_t)max_optin - sp.off_bufs - dev::kOverrunWords * 4;
-            int64_t bb = space / nst / 16 * 16;  // stage bytes
-            if (!es && ec && atoi(ec) != 0) {
-                // stages sized for full 31-slice chunks (consumer warp w <-> slice w)
-                // when at least 4 of them fit
-                uint64_t mxb = 0;
-                for (int64_t q = 0; q < nsl;) {
-                    if (is_long[q]) {
-                        q++;
-                        continue;
-                    }
-                    int64_t k = 1;
-                    while (k < dev::kCtaConsumers && q + k < nsl && !is_long[q + k]) k++;
-                    mxb = std::max(mxb, chunk_bytes(c->directory, q, k));
-                    q += k;
-                }
-                const int64_t fb = (int64_t)((mxb + 15) / 16 * 16);
-                if (fb > 0 && space / fb >= 4) {
-                    bb = fb;
-                    nst = std::min<int64_t>(dev::kMaxCtaStages, space / fb);
-                    h->cta_fixed = true;
-                }
-            }
-            if (!dyn && ec && atoi(ec) != 0 && bb >= (int64_t)sp.bufb && bb / 4 < 65536) {
-                h->cta_mode = true;
-                h->cta_stages = (int)nst;
-                h->cta_bufb = (int)bb;
-                h->cta_smem = (int)(sp.off_bufs + nst * bb + dev::kOverrunWords * 4);
-            }
             int64_t s = 0;
             while (s < nsl) {
                 if (is_long[s]) {
@@ -626,15 +674,9 @@ extern "C" int dtans_upload(const dtans_container_view *c, int device, dtans_dev
                     continue;
                 }
                 int64_t k = 1;
-                if (h->cta_mode) {
-                    while (k < dev::kCtaConsumers && s + k < nsl && !is_long[s + k] &&
-                           chunk_bytes(c->directory, s, k + 1) <= (uint64_t)h->cta_bufb)
-                        k++;
-                } else {
-                    while (k < kcap && s + k < nsl && !is_long[s + k] &&
-                           chunk_bytes(c->directory, s, k + 1) <= (uint64_t)sp.bufb)
-                        k++;
-                }
+                while (k < kcap && s + k < nsl && !is_long[s + k] &&
+                       chunk_bytes(c->directory, s, k + 1) <= (uint64_t)sp.bufb)
+                    k++;
                 push(s, k);
                 s += k;
             }
@@ -687,46 +729,51 @@ extern "C" int dtans_upload(const dtans_container_view *c, int device, dtans_dev
     };
     cp(h->d_tables, sp.image.data(), sp.image.size() * 4);
     {
-        // assemble the chunk blobs on the host (multithreaded) and upload
-        std::vector<uint32_t> blob((size_t)h->blob_words, 0u);
+        // Stream the chunk blobs to the device through pinned staging
+        // buffers: worker threads assemble a batch of consecutive chunks
+        // straight from the caller's arrays (possibly an mmapped CDTA file,
+        // container.py:647-720) into one pinned buffer while the previous
+        // batch's cudaMemcpyAsync runs; no full host copy of the container
+        // is made.  Blobs are laid out in chunk order, so a batch is one
+        // contiguous device range.
         const size_t nch = h->chunks.size();
-        const unsigned nt = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
-        std::vector<std::thread> th;
-        for (unsigned t = 0; t < nt; t++)
-            th.emplace_back([&, t]() {
-                for (size_t q = nch * t / nt; q < nch * (t + 1) / nt; q++) {
-                    const dev::ChunkRec &r = h->chunks[q];
-                    const int64_t s0 = r.s0, k = r.kw & 0xFF;
-                    uint32_t *p = blob.data() + r.off;
-                    const uint64_t base = c->directory[s0];
-                    for (int64_t i = 0; i < k; i++) {
-                        // slice metadata word (kernels.cuh slice_meta)
-                        const int64_t sr0 = (s0 + i) * kSlice;
-                        uint32_t maxn = 0, minseg = 0xFFFFFFFFu;
-                        for (int64_t l = 0; l < kSlice; l++) {
-                            const uint32_t n = sr0 + l < c->rows ? c->row_symbols[sr0 + l] : 0u;
-                            maxn = std::max(maxn, n);
-                            minseg = std::min(minseg, (n + 7u) / 8u);
-                        }
-                        const uint32_t mseg = (maxn + 7u) / 8u;
-                        const uint32_t np = pads_ok && mseg > 0 ? (maxn - 8u * (mseg - 1u)) / 2u : 4u;
-                        p[i] = dev::slice_meta((uint32_t)(c->directory[s0 + i + 1] - base), mseg, minseg, np);
-                    }
-                    p += dev::chunk_hdr_words((uint32_t)k);
-                    const int64_t r0 = s0 * kSlice, r1 = std::min<int64_t>((s0 + k) * kSlice, c->rows);
-                    memcpy(p, c->row_symbols + r0, sizeof(uint32_t) * (size_t)(r1 - r0));
-                    p += k * 32;
-                    memcpy(p, c->stream + base, sizeof(uint32_t) * (size_t)(c->directory[s0 + k] - base));
+        PinnedUploader up;
+        if (rc == DTANS_OK) rc = up.init(device);
+        size_t q = 0;
+        while (rc == DTANS_OK && q < nch) {
+            const uint64_t off0 = h->chunks[q].off;
+            size_t qe = q;
+            while (qe < nch && (h->chunks[qe].off + (h->chunks[qe].kw >> 8) - off0) * 4 <= up.cap) qe++;
+            if (qe == q) {
+                rc = fail(DTANS_E_PARAM, "chunk larger than the upload staging buffer");
+                break;
+            }
+            const uint64_t words = h->chunks[qe - 1].off + (h->chunks[qe - 1].kw >> 8) - off0;
+            uint32_t *dst = (uint32_t *)up.acquire();
+            if (!dst) {
+                rc = cuda_fail(up.err, "upload staging");
+                break;
+            }
+            parallel_for(qe - q, [&](size_t lo, size_t hi) {
+                for (size_t i = lo; i < hi; i++) {
+                    const dev::ChunkRec &r = h->chunks[q + i];
+                    assemble_chunk(c, r, pads_ok, dst + (r.off - off0));
                 }
             });
-        for (auto &t : th) t.join();
-        cp(h->d_blob, blob.data(), blob.size() * 4);
-    }
-    if (need_raw) {
-        cp(h->d_row_symbols, c->row_symbols, sizeof(uint32_t) * (size_t)c->rows);
-        cp(h->d_directory, c->directory, sizeof(uint64_t) * (size_t)(nsl + 1));
-        cp(h->d_stream, c->stream, sizeof(uint32_t) * (size_t)c->nwords);
-        zero(h->d_stream + c->nwords, sizeof(uint32_t) * kRawStreamPad);
+            if (!up.submit(h->d_blob + off0, words * 4)) rc = cuda_fail(up.err, "upload chunk blobs");
+            q = qe;
+        }
+        if (rc == DTANS_OK && need_raw) {
+            // the long-slice kernels read the reference arrays directly
+            if (!up.copy(h->d_row_symbols, c->row_symbols, sizeof(uint32_t) * (size_t)c->rows) ||
+                !up.copy(h->d_directory, c->directory, sizeof(uint64_t) * (size_t)(nsl + 1)) ||
+                !up.copy(h->d_stream, c->stream, sizeof(uint32_t) * (size_t)c->nwords))
+                rc = cuda_fail(up.err, "upload raw arrays");
+            zero(h->d_stream + c->nwords, sizeof(uint32_t) * kRawStreamPad);
+        }
+        if (rc == DTANS_OK && !up.finish()) rc = cuda_fail(up.err, "upload");
+        h->upload_staged_bytes = up.bytes;
+        h->upload_batches = up.batches;
     }
     zero(h->d_err, 64);
     cp(h->d_chunks, h->chunks.data(), sizeof(dev::ChunkRec) * h->chunks.size());
@@ -766,10 +813,9 @@ extern "C" int dtans_upload(const dtans_container_view *c, int device, dtans_dev
     if (getenv("DTANS_VERBOSE"))
         fprintf(stderr,
                 "[dtans] rows=%lld slices=%lld chunks=%zu nring=%d bufb=%d smem=%d dinline=%d rep_d=%d rep_v=%d "
-                "nlong=%u ntasks=%u nsolo=%u dynamic=%d task_smem=%d cta_stages=%d cta_bufb=%d\n",
+                "nlong=%u ntasks=%u nsolo=%u dynamic=%d task_smem=%d\n",
                 (long long)h->rows, (long long)nsl, h->chunks.size(), sp.nring, sp.bufb, h->smem, (int)tb.dinline,
-                tb.rep_d, tb.rep_v, h->base.nlong, h->base.ntasks, h->base.nsolo, h->base.dynamic, h->task_smem,
-                h->cta_mode ? h->cta_stages : 0, h->cta_bufb);
+                tb.rep_d, tb.rep_v, h->base.nlong, h->base.ntasks, h->base.nsolo, h->base.dynamic, h->task_smem);
     *out = h;
     return DTANS_OK;
 }
@@ -870,6 +916,8 @@ extern "C" int dtans_plan(const dtans_dev *h, dtans_plan_t *out)
     out->dinline = h->dinline ? 1 : 0;
     out->bufb = h->base.bufb;
     out->nring = h->base.nring;
+    out->upload_bytes = (int64_t)h->upload_staged_bytes;
+    out->upload_batches = h->upload_batches;
     return DTANS_OK;
 }
 

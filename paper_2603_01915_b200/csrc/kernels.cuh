@@ -50,11 +50,8 @@ constexpr int kSlots = 4096;
 #ifndef DTANS_TASK_WARPS
 #define DTANS_TASK_WARPS 32
 #endif
-#ifndef DTANS_CTA_WARPS
-#define DTANS_CTA_WARPS 32
-#endif
-constexpr int kMaxWarps = DTANS_CTA_WARPS;  // warps per CTA of the main kernel
-constexpr int kMaxRing = 3;     // staging buffers per warp (runtime 2 or 3)
+constexpr int kMaxWarps = 32;  // warps per CTA of the main kernel
+constexpr int kMaxRing = 2;     // staging buffers per warp (a double-buffered ring)
 constexpr int kMaxChunk = 16;   // slices per chunk
 constexpr uint32_t kTabBytes = 2 * kSlots * 4;
 constexpr uint32_t kDeltaInlineEsc = 0xFFFF0000u;  // inline deltas: F = 0xFFFF marks an escape
@@ -112,7 +109,7 @@ struct KernelArgs {
     int32_t pads_ok;              // both domains retain a pad symbol
     int32_t off_bars, off_meta, off_ctl, off_bufs;  // shared-memory layout
     int32_t bufb;                 // bytes per staging buffer (multiple of 16)
-    int32_t nring;                // staging buffers per warp (2 or 3)
+    int32_t nring;                // staging buffers per warp (kMaxRing)
     const uint32_t *blob;         // chunk blobs (main kernel)
     const uint32_t *row_symbols;  // rows (long-slice kernels only)
     const uint64_t *directory;    // nslices + 1 (long-slice kernels only)
@@ -144,8 +141,6 @@ struct KernelArgs {
     uint32_t chunk_lo, chunk_hi;  // chunks of this launch
     int32_t dynamic;              // 1: atomic ticket counter instead of a static stride
     uint32_t *work_counter;       // zeroed before every dynamic launch
-    int32_t nstages;              // CTA-pipelined kernel: stage buffers of bufb bytes in the CTA ring
-    int32_t cta_fixed;            // stages sized for full chunks: consumer warp w <-> slice w
 };
 
 __device__ __forceinline__ uint32_t lanemask_lt()
@@ -749,19 +744,7 @@ __device__ __forceinline__ void init_state(const Ctx &C, Src &src, const uint32_
 template <typename V> __device__ __forceinline__ V ld_stream(const V *p)
 {
 #if DTANS_YSTREAM
-    V v;
-    if (sizeof(V) == 8) {
-        unsigned long long b;
-        asm("{\n.reg .b64 pol;\ncreatepolicy.fractional.L2::evict_first.b64 pol, 1.0;\n"
-            "ld.global.nc.L1::no_allocate.L2::cache_hint.b64 %0, [%1], pol;\n}" : "=l"(b) : "l"(p));
-        memcpy(&v, &b, 8);
-    } else {
-        uint32_t b;
-        asm("{\n.reg .b64 pol;\ncreatepolicy.fractional.L2::evict_first.b64 pol, 1.0;\n"
-            "ld.global.nc.L1::no_allocate.L2::cache_hint.b32 %0, [%1], pol;\n}" : "=r"(b) : "l"(p));
-        memcpy(&v, &b, 4);
-    }
-    return v;
+    return __ldcs(p);  // ld.global.cs: evict-first in L1 and L2, no policy register
 #else
     return __ldg(p);
 #endif
@@ -843,6 +826,14 @@ __device__ __forceinline__ uint2 ld_shared_v2(uint32_t addr)
     return v;
 }
 
+// 16-byte global -> shared copy that does not hold a register (LDGSTS):
+// lane 0 prefetches the next chunk record a whole chunk ahead of its use.
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void *src)
+{
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\ncp.async.commit_group;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
 // Chunk staging (lane 0): one cp.async.bulk of the chunk's blob completing
 // on the buffer's mbarrier.  The previous contents were consumed by this
 // warp's LDS before the __syncwarp that precedes the call (the same WAR
@@ -886,7 +877,7 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) dtans_kernel(const KernelAr
     const uint32_t metas = sb + (uint32_t)a.off_meta + (uint32_t)warp * kMaxRing * 8u;
     WarpCtl *ctl = reinterpret_cast<WarpCtl *>(dtans_smem + a.off_ctl) + warp;
     if (lane == 0) {
-        for (int b = 0; b < a.nring; b++) mbar_init(bars + 8u * b, 1);
+        for (int b = 0; b < kMaxRing; b++) mbar_init(bars + 8u * b, 1);
         fence_mbar_init();
     }
     __syncthreads();
@@ -906,17 +897,19 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) dtans_kernel(const KernelAr
         if (a.sumsq_zero != nullptr && blockIdx.x == 0 && threadIdx.x == 0) *a.sumsq_zero = 0.0;
     }
 
-    // lane 0's claim pipeline: ticket -> chunk record -> staged buffer
+    // lane 0's claim pipeline: ticket -> chunk record (cp.async into the
+    // control block, a chunk ahead) -> staged buffer
     auto claim = [&]() -> uint32_t {  // lane 0 only; >= chunk_hi: none
         if (a.dynamic) return a.chunk_lo + atomicAdd(a.work_counter, 1u);
         const uint32_t c = ctl->next_static;
         ctl->next_static = c + gridDim.x * kWarps;
         return c;
     };
+    const uint32_t ctl_sh = sb + (uint32_t)a.off_ctl + (uint32_t)warp * (uint32_t)sizeof(WarpCtl);
+    const uint32_t bufs = sb + (uint32_t)a.off_bufs + (uint32_t)warp * (uint32_t)(kMaxRing * a.bufb);
     if (lane == 0) {
         ctl->next_static = a.chunk_lo + blockIdx.x * kWarps + warp;
-        const uint32_t bufs = sb + (uint32_t)a.off_bufs + (uint32_t)warp * (uint32_t)a.nring * (uint32_t)a.bufb;
-        for (int b = 0; b < a.nring; b++) {
+        for (int b = 0; b < kMaxRing; b++) {
             const uint32_t c = claim();
             const bool v = c < a.chunk_hi;
             ChunkRec rc{};
@@ -925,23 +918,22 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) dtans_kernel(const KernelAr
         }
         const uint32_t c = claim();
         ctl->pend_ok = c < a.chunk_hi;
-        if (c < a.chunk_hi) ctl->pend = a.chunks[c];
+        if (c < a.chunk_hi) cp_async16(ctl_sh, a.chunks + c);
         ctl->pend_c = claim();
     }
     __syncwarp();
-    uint32_t b = 0, parity = 0;
-    for (;;) {
-        mbar_wait(bars + 8u * b, parity);
+    for (uint32_t it = 0;; it++) {
+        const uint32_t b = it & (kMaxRing - 1u);
+        mbar_wait(bars + 8u * b, (it / kMaxRing) & 1u);
         const uint2 md = ld_shared_v2(metas + 8u * b);
         const uint32_t s0 = md.x, k = md.y;
         if (k == 0) break;  // uniform: this warp's chunks are exhausted
         // the chunk's addresses live in the warp's control block and are
         // re-read per slice (one LDS.128) instead of occupying registers
         // across the decode
-        const uint32_t ctl_cs = sb + (uint32_t)a.off_ctl + (uint32_t)warp * (uint32_t)sizeof(WarpCtl) + 32u;
+        const uint32_t ctl_cs = ctl_sh + 32u;
         if (lane == 0) {
-            const uint32_t buf =
-                sb + (uint32_t)a.off_bufs + ((uint32_t)warp * (uint32_t)a.nring + b) * (uint32_t)a.bufb;
+            const uint32_t buf = bufs + b * (uint32_t)a.bufb;
             const uint32_t hw = chunk_hdr_words(k);
             st_shared_v4(ctl_cs, buf, buf + hw * 4u, buf + (hw + k * 32u) * 4u, s0);
         }
@@ -957,141 +949,16 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) dtans_kernel(const KernelAr
                                                             (cs.w + i) * kSliceRows + (uint32_t)lane, lane, scale, wsum);
             dcur = dnext;
         }
-        const uint32_t buf = ld_shared_v4(ctl_cs).x;
         __syncwarp();
         if (lane == 0) {
-            stage_chunk(a, ctl->pend_ok != 0u, ctl->pend, bars + 8u * b, metas + 8u * b, buf);
+            cp_async_wait_all();  // the pending record (issued a chunk ago)
+            stage_chunk(a, ctl->pend_ok != 0u, ctl->pend, bars + 8u * b, metas + 8u * b, bufs + b * (uint32_t)a.bufb);
             const uint32_t c = ctl->pend_c;
             ctl->pend_ok = c < a.chunk_hi;
-            if (c < a.chunk_hi) ctl->pend = a.chunks[c];
+            if (c < a.chunk_hi) cp_async16(ctl_sh, a.chunks + c);
             ctl->pend_c = claim();
         }
         __syncwarp();
-        if (++b == (uint32_t)a.nring) {
-            b = 0;
-            parity ^= 1u;
-        }
-    }
-    if (kScaled && a.sumsq_out != nullptr) {
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) wsum = __dadd_rn(wsum, __shfl_xor_sync(0xFFFFFFFFu, wsum, o));
-        if (lane == 0) atomicAdd(a.sumsq_out, wsum);
-    }
-}
-
-// CTA-pipelined variant of the main kernel: one producer warp (lane 0)
-// stages whole chunks of up to kCtaConsumers slices into a ring of
-// `nstages` CTA-wide buffers with one bulk copy each; the consumer warps
-// deal the chunks' slices round-robin.  Per slice the consumers pay a few
-// shared loads, and per stage one mbarrier wait and one arrive, instead of a
-// per-warp claim/stage pipeline per few slices.
-// Full barriers: the producer's arrive.expect_tx + the copy's complete_tx.
-// Empty barriers: one arrive per consumer warp.  The producer ends the
-// sequence with an empty chunk (k = 0) that every consumer reads as "done".
-constexpr int kCtaConsumers = kMaxWarps - 1;
-constexpr int kMaxCtaStages = kMaxWarps * kMaxRing / 2;  // full + empty barriers fit the bars region
-
-template <typename V, bool kDecode, bool kHasY, bool kDIn, bool kScaled = false>
-__global__ void __launch_bounds__(kMaxWarps * 32, 1) dtans_cta_kernel(const KernelArgs a)
-{
-    const bool aligned = load_tables(a);
-    const int lane = threadIdx.x & 31;
-    const int warp = threadIdx.x >> 5;
-    const uint32_t sb = smem_u32(dtans_smem);
-    const uint32_t S = (uint32_t)a.nstages;
-    const uint32_t full = sb + (uint32_t)a.off_bars, empty = full + 8u * kMaxCtaStages;
-    const uint32_t metas = sb + (uint32_t)a.off_meta;
-    const uint32_t bufs = sb + (uint32_t)a.off_bufs;
-    if (threadIdx.x == 0) {
-        for (uint32_t q = 0; q < S; q++) {
-            mbar_init(full + 8u * q, 1);
-            mbar_init(empty + 8u * q, kCtaConsumers);
-        }
-        fence_mbar_init();
-    }
-    __syncthreads();
-    if (!aligned) {
-        if (threadIdx.x == 0) atomicOr(a.err, 4u);
-        return;
-    }
-    if (warp == kCtaConsumers) {  // producer
-        if (lane == 0) {
-            for (uint32_t i = 0;; i++) {
-                const uint32_t slot = i % S, use = i / S;
-                if (use > 0) mbar_wait(empty + 8u * slot, (use - 1u) & 1u);
-                const uint32_t c = a.chunk_lo + blockIdx.x + i * gridDim.x;
-                const bool v = c < a.chunk_hi;
-                ChunkRec rc{};
-                if (v) rc = a.chunks[c];
-                stage_chunk(a, v, rc, full + 8u * slot, metas + 8u * slot, bufs + slot * (uint32_t)a.bufb);
-                if (!v) break;
-            }
-        }
-        return;
-    }
-    const Ctx C = make_ctx<V>(a, lane);
-    const V *__restrict__ x = reinterpret_cast<const V *>(a.x);
-    V scale = V(1);
-    double wsum = 0.0;
-    if (kScaled) {
-        if (a.sumsq_in != nullptr) {
-            const double q = *a.sumsq_in;
-            scale = (V)__ddiv_rn(1.0, __dsqrt_rn(q));
-        }
-        if (a.sumsq_zero != nullptr && blockIdx.x == 0 && threadIdx.x == 0) *a.sumsq_zero = 0.0;
-    }
-    if (a.cta_fixed) {
-        // stages sized for full chunks: consumer w decodes slice w of each
-        for (uint32_t i = 0;; i++) {
-            const uint32_t slot = i % S;
-            mbar_wait(full + 8u * slot, (i / S) & 1u);
-            const uint2 md = ld_shared_v2(metas + 8u * slot);
-            const uint32_t k = md.y;
-            if (k == 0) break;  // uniform: the producer's end marker
-            if ((uint32_t)warp < k) {
-                const uint32_t w = (uint32_t)warp;
-                const uint32_t buf = bufs + slot * (uint32_t)a.bufb;
-                const uint32_t hw = chunk_hdr_words(k);
-                const uint32_t meta = sh32(buf + 4u * w);
-                const uint32_t dstart = w ? (sh32(buf + 4u * w - 4u) & 0xFFFFu) : 0u;
-                const uint32_t n = sh32(buf + (hw + w * 32u + (uint32_t)lane) * 4u);
-                const SmemSrc src{buf + (hw + k * 32u + dstart) * 4u};
-                decode_slice<V, kDecode, kHasY, kDIn, kScaled>(a, C, x, src, (meta & 0xFFFFu) - dstart, meta, n,
-                                                                (md.x + w) * kSliceRows + (uint32_t)lane, lane,
-                                                                scale, wsum);
-            }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(empty + 8u * slot);
-        }
-    } else {
-    // consumer w takes the CTA's slices w, w + kCtaConsumers, ... across the
-    // stage sequence (stages hold k <= kCtaConsumers slices each) and
-    // releases every stage once, when it moves past it
-    uint32_t i = 0, slot = 0, base = 0;
-    mbar_wait(full, 0u);
-    uint2 md = ld_shared_v2(metas);
-    for (uint32_t g = (uint32_t)warp; md.y != 0u; g += kCtaConsumers) {
-        while (g >= base + md.y) {
-            __syncwarp();
-            if (lane == 0) mbar_arrive(empty + 8u * slot);
-            base += md.y;
-            i++;
-            slot = i % S;
-            mbar_wait(full + 8u * slot, (i / S) & 1u);
-            md = ld_shared_v2(metas + 8u * slot);
-            if (md.y == 0u) break;  // uniform: the producer's end marker
-        }
-        if (md.y == 0u) break;
-        const uint32_t k = md.y, w = g - base;
-        const uint32_t buf = bufs + slot * (uint32_t)a.bufb;
-        const uint32_t hw = chunk_hdr_words(k);
-        const uint32_t meta = sh32(buf + 4u * w);
-        const uint32_t dstart = w ? (sh32(buf + 4u * w - 4u) & 0xFFFFu) : 0u;
-        const uint32_t n = sh32(buf + (hw + w * 32u + (uint32_t)lane) * 4u);
-        const SmemSrc src{buf + (hw + k * 32u + dstart) * 4u};
-        decode_slice<V, kDecode, kHasY, kDIn, kScaled>(a, C, x, src, (meta & 0xFFFFu) - dstart, meta, n,
-                                                        (md.x + w) * kSliceRows + (uint32_t)lane, lane, scale, wsum);
-    }
     }
     if (kScaled && a.sumsq_out != nullptr) {
 #pragma unroll

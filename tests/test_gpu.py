@@ -214,13 +214,11 @@ def _host_vs_device(c, x, y, stages=None, monkeypatch=None):
     return out, ref
 
 
-@pytest.mark.parametrize("cta", ["0", "1"])
 @pytest.mark.parametrize("stages", [1, 8, 32])
 @pytest.mark.parametrize("gen", ["laplacian", "banded", "random"])
-def test_host_buffer_path_matches_device_path(gen, stages, cta, monkeypatch):
+def test_host_buffer_path_matches_device_path(gen, stages, monkeypatch):
     """dtans_spmv_host (pipelined H2D / kernel on chunk ranges / D2H) equals
-    the device-pointer path bitwise, with either main kernel."""
-    monkeypatch.setenv("DTANS_CTA", cta)
+    the device-pointer path bitwise."""
     m = {"laplacian": lambda: synth.laplacian_2d(700),
          "banded": lambda: synth.banded(200000, 27, levels=256, seed=4),
          "random": lambda: synth.config1_random(20000, 300000, seed=3)}[gen]()
@@ -280,34 +278,3 @@ def test_nccl_power_iteration_rejects_bad_layout():
     with pytest.raises(P.ParameterError):
         comm.power_iteration(dev, [0, m.rows - 1], x0, 3)
     comm.close()
-
-
-@pytest.mark.parametrize("stages", ["2", "6", "16"])
-@pytest.mark.parametrize("gen", ["laplacian", "banded", "rmat_sorted", "random"])
-def test_cta_pipelined_kernel_bitwise(gen, stages, monkeypatch):
-    """The opt-in CTA-wide producer/consumer kernel (DTANS_CTA=1) is bitwise
-    the per-warp ring kernel, for SpMV, y-less SpMV and decode."""
-    m = {"laplacian": lambda: synth.laplacian_2d(500),
-         "banded": lambda: synth.banded(120000, 27, levels=256, seed=4),
-         "rmat_sorted": lambda: P.sort_rows_by_length(synth.rmat(14, 16 << 14))[0],
-         "random": lambda: synth.config1_random(20000, 300000, seed=3)}[gen]()
-    x, y = synth.vectors(m)
-    c = P.encode_matrix(m)
-    V = np.float64 if c.precision == 8 else np.float32
-    xt = torch.from_numpy(np.ascontiguousarray(x, V)).cuda()
-    yt = torch.from_numpy(np.ascontiguousarray(y, V)).cuda()
-    outs = []
-    for cta in ("0", "1"):
-        monkeypatch.setenv("DTANS_CTA", cta)
-        monkeypatch.setenv("DTANS_CTA_STAGES", stages)
-        dc = c.device(0)
-        outs.append((dc.spmv(xt, yt).cpu().numpy(), dc.spmv(xt, None).cpu().numpy()))
-        dc.close()
-    assert G.same_bits_or_nan(outs[0][0], outs[1][0])
-    assert G.same_bits_or_nan(outs[0][1], outs[1][1])
-    decoded = []
-    for cta in ("0", "1"):  # decode instantiations of both kernels
-        monkeypatch.setenv("DTANS_CTA", cta)
-        decoded.append(P.decode_matrix(c))
-        c.device(0).close()
-    assert decoded[0] == decoded[1]

@@ -186,3 +186,26 @@ def test_fused_power_iteration_with_long_slices(dtype, monkeypatch):
     tol = 1e-12 if dtype == np.float64 else 1e-5
     assert abs(lf - lu) <= 10 * tol * lu
     assert np.allclose(xf.cpu().numpy(), xu.cpu().numpy(), rtol=100 * tol, atol=100 * tol / np.sqrt(m.cols))
+
+
+@pytest.mark.parametrize("gen", ["laplacian700", "rmat14_f32"])
+def test_streamed_upload_from_mmapped_file(gen, tmp_path, monkeypatch):
+    """dtans_upload streams the chunk blobs (and, with long slices, the raw
+    arrays) through pinned staging buffers straight from a mmapped CDTA
+    file (container.py:647-720): many small batches (DTANS_UPLOAD_KB=64)
+    give the same product as the oracle, bitwise."""
+    monkeypatch.setenv("DTANS_UPLOAD_KB", "64")
+    m = MID[gen]()
+    x, y = synth.vectors(m)
+    c0 = P.encode_matrix(m)
+    path = tmp_path / "m.cdta"
+    P.save(c0, str(path))
+    c = P.load(str(path))
+    dc = c.device(0)
+    plan = dc.plan()
+    assert plan["upload_batches"] >= 4, plan
+    out = P.spmv(c, x, y)
+    ref = O.spmv(O.parse(P.serialize(c0)), x, y, threads=8)
+    assert G.check_spmv(out, ref, m, x, y)
+    assert P.decode_matrix(c) == P.CsrMatrix(m.rows, m.cols, m.row_start, m.col_idx,
+                                             m.values.astype(c.value_dtype))

@@ -45,7 +45,9 @@ def main():
         c.row_map = perm
     t_enc = time.time() - t0
     x, y = spec.vectors(0, spec.rows)
+    t0 = time.time()
     dc = c.device(0)
+    t_up = time.time() - t0
     xt = torch.from_numpy(x).cuda()
     yt = None if a.noy else torch.from_numpy(y).cuda()
     out = torch.empty(m.rows, dtype=xt.dtype, device="cuda")
@@ -89,7 +91,7 @@ def main():
         os.path.join(REPO, "MEASURED_PEAKS.json")) else 6650.0
     tw = float(np.median(warm))
     tc = float(np.median(cold))
-    res = {"config": a.config, "scale": a.scale, "reorder": a.reorder, "nnz": int(m.nnz), "encode_s": round(t_enc, 1),
+    res = {"config": a.config, "scale": a.scale, "reorder": a.reorder, "nnz": int(m.nnz), "encode_s": round(t_enc, 1), "upload_s": round(t_up, 3),
            "warm_ms": round(tw, 5), "cold_ms": round(tc, 5), "frac_warm": round(alg / (tw * 1e-3) / 1e9 / pk, 4),
            "frac_cold": round(alg / (tc * 1e-3) / 1e9 / pk, 4), "plan": dc.plan()}
     if a.check:
