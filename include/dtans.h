@@ -232,8 +232,15 @@ typedef struct {
     int32_t bufb, nring;      /* staging buffer bytes, buffers per warp */
     int64_t upload_bytes;     /* bytes streamed through the pinned upload buffers */
     int64_t upload_batches;   /* cudaMemcpyAsync batches of the upload */
+    int64_t nstaged;          /* long-slice tasks the main kernel decodes from shared memory */
 } dtans_plan_t;
 int dtans_plan(const dtans_dev *h, dtans_plan_t *out);
+
+/* Slices whose rows are summed from several task partials (long slices cut
+ * into segment ranges): their y' matches the reference within the
+ * north-star tolerance, every other row bitwise.  Writes up to cap slice
+ * indices (ascending) to out (may be NULL); returns how many there are. */
+int64_t dtans_split_slices(const dtans_dev *h, uint32_t *out, int64_t cap);
 
 #ifdef __cplusplus
 }

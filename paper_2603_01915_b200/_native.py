@@ -26,7 +26,7 @@ EXPORTS = (
     "dtans_spmv_f32", "dtans_spmv_host", "dtans_decode", "dtans_check",
     "dtans_launch_count", "dtans_set_row_map", "dtans_spmv_scaled", "dtans_set_col_map",
     "dtans_encode_device", "dtans_mg_unique_id", "dtans_mg_init", "dtans_mg_free", "dtans_mg_power_iteration",
-    "dtans_plan",
+    "dtans_plan", "dtans_split_slices",
 )
 
 
@@ -74,6 +74,7 @@ class Plan(ctypes.Structure):
         ("dynamic", ctypes.c_int32), ("dinline", ctypes.c_int32),
         ("bufb", ctypes.c_int32), ("nring", ctypes.c_int32),
         ("upload_bytes", ctypes.c_int64), ("upload_batches", ctypes.c_int64),
+        ("nstaged", ctypes.c_int64),
     ]
 
 
@@ -118,6 +119,8 @@ def lib() -> ctypes.CDLL:
     L.dtans_launch_count.argtypes = [vp]
     L.dtans_launch_count.restype = i64
     L.dtans_plan.argtypes = [vp, ctypes.POINTER(Plan)]
+    L.dtans_split_slices.restype = ctypes.c_int64
+    L.dtans_split_slices.argtypes = [vp, vp, ctypes.c_int64]
     _lib = L
     return L
 

@@ -286,6 +286,25 @@ class DeviceContainer:
         _native.check(_native.lib().dtans_plan(self.handle, ctypes.byref(p)))
         return {k: getattr(p, k) for k, _ in _native.Plan._fields_}
 
+    def split_slices(self) -> np.ndarray:
+        """Slices whose rows sum several task partials (dtans_split_slices):
+        their y' matches the reference within the north-star tolerance,
+        every other row bitwise."""
+        lib = _native.lib()
+        n = int(lib.dtans_split_slices(self.handle, None, 0))
+        out = np.zeros(max(n, 1), dtype=np.uint32)
+        if n:
+            lib.dtans_split_slices(self.handle, out.ctypes.data, n)
+        return out[:n]
+
+    def split_rows(self, rows: int) -> np.ndarray:
+        """Boolean mask of the rows in split slices."""
+        m = np.zeros(-(-rows // 32) * 32, dtype=bool)
+        s = self.split_slices().astype(np.int64)
+        if len(s):
+            m[(s[:, None] * 32 + np.arange(32)).ravel()] = True
+        return m[:rows]
+
     def launches(self) -> int:
         return int(_native.lib().dtans_launch_count(self.handle))
 

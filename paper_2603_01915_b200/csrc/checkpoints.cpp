@@ -61,96 +61,84 @@ void parse_tables(const uint8_t *recs, int precision, HostTables &t)
     t.pw[1] = (uint8_t)(precision / 4);
 }
 
-// Walk one slice; append checkpoints for segments chunk, 2*chunk, ...
-// Returns false on a corrupt slice (reads past the stream or consumption
-// mismatch).  Column deltas need the symbols, so escapes' payloads and the
-// delta dictionary are read like the device does.
-bool walk_slice(const dtans_container_view *c, const HostTables &T, const uint32_t *dsym_tab, int64_t s,
-                int chunk, std::vector<uint32_t> &pool, std::vector<LongTask> &tasks, std::vector<SoloTask> &solo,
-                uint32_t part_base)
-{
-    const int64_t row0 = s * kSlice;
-    const int nl = (int)std::min<int64_t>(kSlice, c->rows - row0);
-    const uint64_t lo = c->directory[s], hi = c->directory[s + 1];
-    const uint32_t *st = c->stream + lo;
-    const uint64_t nw = hi - lo;
+// Lockstep replay of one slice on the host: the lanes' resume state at the
+// current segment start and the slice cursor (container.py:406-497).
+struct SliceWalk {
+    const dtans_container_view *c;
+    const HostTables &T;
+    const uint32_t *dsym_tab;
+    int nl = 0;
+    const uint32_t *st = nullptr;
+    uint64_t nw = 0, cur = 0;
     uint32_t n[kSlice] = {0}, nseg[kSlice] = {0};
     uint32_t w0[kSlice] = {0}, w1[kSlice] = {0}, w2[kSlice] = {0}, d[kSlice] = {0}, r[kSlice], col[kSlice] = {0};
     uint32_t max_nseg = 0;
-    for (int i = 0; i < kSlice; i++) r[i] = 1;
-    for (int i = 0; i < nl; i++) {
-        n[i] = c->row_symbols[row0 + i];
-        nseg[i] = (n[i] + 7) / 8;
-        max_nseg = std::max(max_nseg, nseg[i]);
+
+    SliceWalk(const dtans_container_view *cv, const HostTables &t, const uint32_t *ds, int64_t s)
+        : c(cv), T(t), dsym_tab(ds)
+    {
+        const int64_t row0 = s * kSlice;
+        nl = (int)std::min<int64_t>(kSlice, c->rows - row0);
+        const uint64_t lo = c->directory[s], hi = c->directory[s + 1];
+        st = c->stream + lo;
+        nw = hi - lo;
+        for (int i = 0; i < kSlice; i++) r[i] = 1;
+        for (int i = 0; i < nl; i++) {
+            n[i] = c->row_symbols[row0 + i];
+            nseg[i] = (n[i] + 7) / 8;
+            max_nseg = std::max(max_nseg, nseg[i]);
+        }
     }
-    uint64_t cur = 0;
-    auto fetch = [&](uint32_t &dst) -> bool {
+    bool fetch(uint32_t &dst)
+    {
         if (cur >= nw) return false;
         dst = st[cur++];
         return true;
-    };
-    for (int i = 0; i < nl; i++)
-        if (nseg[i] && !fetch(w0[i])) return false;
-    for (int i = 0; i < nl; i++)
-        if (nseg[i] && !fetch(w1[i])) return false;
-    for (int i = 0; i < nl; i++)
-        if (nseg[i] && !fetch(w2[i])) return false;
-    const uint32_t ntasks = (max_nseg + chunk - 1) / chunk;
-    uint32_t k = 0;
-    const size_t first_task = tasks.size(), first_solo = solo.size();
-    for (uint32_t j = 0; j < max_nseg; j++) {
-        uint32_t amask = 0;
-        if (j % chunk == 0 && j)
-            for (int i = 0; i < nl; i++)
-                if (nseg[i] > j) amask |= 1u << i;
-        if (j % chunk == 0 && j && __builtin_popcount(amask) == 1) {
-            // one lane left: its remaining words are consecutive (solo task)
-            const int i = __builtin_ctz(amask);
-            SoloTask t;
-            t.slice = (uint32_t)s;
-            t.lane = (uint32_t)i;
-            t.j0 = j;
-            t.j1 = std::min<uint32_t>(j + chunk, max_nseg);
-            t.part = part_base + k;
-            t.cur0 = (uint32_t)cur;
-            t.cur1 = 0;
-            t.ck = (uint32_t)pool.size();
-            pool.push_back(w0[i]);
-            pool.push_back(w1[i]);
-            pool.push_back(w2[i]);
-            pool.push_back(d[i]);
-            pool.push_back(r[i]);
-            pool.push_back(col[i]);
-            solo.push_back(t);
-            k++;
-        } else if (j % chunk == 0) {
-            // task k covers segments [j, min(j + chunk, max_nseg))
-            LongTask t;
-            t.slice = (uint32_t)s;
-            t.j0 = j;
-            t.j1 = std::min<uint32_t>(j + chunk, max_nseg);
-            t.part = part_base + k;
-            t.cur0 = (uint32_t)cur;
-            t.ck = j == 0 ? 0xFFFFFFFFu : (uint32_t)pool.size();
-            t.last = k + 1 == ntasks;
-            if (j) {
-                uint32_t mask = 0;
-                for (int i = 0; i < nl; i++)
-                    if (nseg[i] > j) mask |= 1u << i;
-                pool.push_back(mask);
-                for (int i = 0; i < nl; i++)
-                    if (mask >> i & 1u) {
-                        pool.push_back(w0[i]);
-                        pool.push_back(w1[i]);
-                        pool.push_back(w2[i]);
-                        pool.push_back(d[i]);
-                        pool.push_back(r[i]);
-                        pool.push_back(col[i]);
-                    }
+    }
+    // init events (container.py:426-429)
+    bool init()
+    {
+        for (int i = 0; i < nl; i++)
+            if (nseg[i] && !fetch(w0[i])) return false;
+        for (int i = 0; i < nl; i++)
+            if (nseg[i] && !fetch(w1[i])) return false;
+        for (int i = 0; i < nl; i++)
+            if (nseg[i] && !fetch(w2[i])) return false;
+        return true;
+    }
+    uint32_t active_mask(uint32_t j) const
+    {
+        uint32_t m = 0;
+        for (int i = 0; i < nl; i++)
+            if (nseg[i] > j) m |= 1u << i;
+        return m;
+    }
+    // the resume record {mask, per active lane w0, w1, w2, d, r, col}
+    void push_ck(std::vector<uint32_t> &pool, uint32_t mask) const
+    {
+        pool.push_back(mask);
+        for (int i = 0; i < nl; i++)
+            if (mask >> i & 1u) {
+                pool.push_back(w0[i]);
+                pool.push_back(w1[i]);
+                pool.push_back(w2[i]);
+                pool.push_back(d[i]);
+                pool.push_back(r[i]);
+                pool.push_back(col[i]);
             }
-            tasks.push_back(t);
-            k++;
-        }
+    }
+    void push_lane(std::vector<uint32_t> &pool, int i) const
+    {
+        pool.push_back(w0[i]);
+        pool.push_back(w1[i]);
+        pool.push_back(w2[i]);
+        pool.push_back(d[i]);
+        pool.push_back(r[i]);
+        pool.push_back(col[i]);
+    }
+    // segment j: payload event, the two checks, the unconditional load
+    bool step(uint32_t j)
+    {
         uint32_t slot[kSlice][8];
         for (int i = 0; i < nl; i++) {
             if (j >= nseg[i]) continue;
@@ -199,29 +187,143 @@ bool walk_slice(const dtans_container_view *c, const HostTables &T, const uint32
         }
         for (int i = 0; i < nl; i++)
             if (j + 1 < nseg[i] && !fetch(w2[i])) return false;
-        // the next task's start cursor
+        return true;
     }
-    // expected cursor at each task end = the next task's start, last = nwords
-    // (warp tasks precede the solo tasks of the same slice)
-    std::vector<uint32_t *> ends;
-    std::vector<uint32_t> starts;
-    for (size_t t = first_task; t < tasks.size(); t++) {
-        ends.push_back(&tasks[t].cur1);
-        starts.push_back(tasks[t].cur0);
+};
+
+// Everything one slice contributes to the index (parts are slice-local
+// until the merge).
+struct SliceOut {
+    std::vector<LongTask> tasks;
+    std::vector<SoloTask> solo;
+    std::vector<StagedTask> staged;
+    std::vector<uint32_t> pool;  // slice-local offsets
+    uint32_t nparts = 0;
+};
+
+void emit_solo(SliceWalk &W, int lane, uint32_t j, int chunk, SliceOut &o)
+{
+    SoloTask t;
+    t.slice = 0;
+    t.lane = (uint32_t)lane;
+    t.j0 = j;
+    t.j1 = std::min<uint32_t>(j + chunk, W.max_nseg);
+    t.part = o.nparts++;
+    t.cur0 = (uint32_t)W.cur;
+    t.cur1 = 0;
+    t.ck = (uint32_t)o.pool.size();
+    W.push_lane(o.pool, lane);
+    o.solo.push_back(t);
+}
+
+// Global-memory tasks of `chunk` segments (and solo tasks once one lane is
+// left at a task boundary).
+bool walk_fixed(SliceWalk &W, int chunk, SliceOut &o)
+{
+    if (!W.init()) return false;
+    const uint32_t ntasks = (W.max_nseg + chunk - 1) / chunk;
+    for (uint32_t j = 0; j < W.max_nseg; j++) {
+        if (j % chunk == 0) {
+            const uint32_t amask = j ? W.active_mask(j) : 0u;
+            if (j && __builtin_popcount(amask) == 1) {
+                emit_solo(W, __builtin_ctz(amask), j, chunk, o);
+            } else {
+                LongTask t;
+                t.slice = 0;
+                t.j0 = j;
+                t.j1 = std::min<uint32_t>(j + chunk, W.max_nseg);
+                t.part = o.nparts++;
+                t.cur0 = (uint32_t)W.cur;
+                t.cur1 = 0;
+                t.ck = j == 0 ? 0xFFFFFFFFu : (uint32_t)o.pool.size();
+                t.last = t.part + 1 == ntasks;
+                if (j) W.push_ck(o.pool, amask);
+                o.tasks.push_back(t);
+            }
+        }
+        if (!W.step(j)) return false;
     }
-    for (size_t t = first_solo; t < solo.size(); t++) {
-        ends.push_back(&solo[t].cur1);
-        starts.push_back(solo[t].cur0);
+    return W.cur == W.nw;
+}
+
+// Words a staged task's blob needs besides its window (api.cu
+// staged_blob_words): header, the 32 row_symbols, the resume record.
+uint64_t staged_fixed_words(uint32_t mask, bool from_init)
+{
+    return 8 + 32 + (from_init ? 0 : ((2 + 6 * (uint64_t)__builtin_popcount(mask) + 3) & ~3ull));
+}
+
+// Staged tasks cut where the blob would overflow stage_words.  Returns 1 on
+// success, 0 on a corrupt slice, -1 if one segment alone does not fit (the
+// caller falls back to walk_fixed).
+int walk_staged(SliceWalk &W, int chunk, uint64_t stage_words, SliceOut &o)
+{
+    if (!W.init()) return 0;
+    uint32_t tj0 = 0, tmask = 0;
+    uint64_t tcur0 = 0;
+    bool tinit = true;
+    std::vector<uint32_t> snap;  // resume record at the current segment start
+    auto fits = [&](uint64_t cur1) {
+        return staged_fixed_words(tmask, tinit) + ((cur1 - tcur0 + 3) & ~3ull) <= stage_words;
+    };
+    auto close = [&](uint32_t j1, uint64_t cur1, const std::vector<uint32_t> *ck) {
+        StagedTask t;
+        t.slice = 0;
+        t.j0 = tj0;
+        t.j1 = j1;
+        t.part = o.nparts++;
+        t.cur0 = (uint32_t)tcur0;
+        t.cur1 = (uint32_t)cur1;
+        t.last = j1 == W.max_nseg;
+        t.ck = 0xFFFFFFFFu;
+        if (ck) {
+            t.ck = (uint32_t)o.pool.size();
+            o.pool.insert(o.pool.end(), ck->begin(), ck->end());
+        }
+        o.staged.push_back(t);
+    };
+    std::vector<uint32_t> tck;  // resume record of the open task
+    for (uint32_t j = 0; j < W.max_nseg; j++) {
+        const uint32_t amask = W.active_mask(j);
+        if (j > 0 && __builtin_popcount(amask) == 1) {
+            const int lane = __builtin_ctz(amask);
+            if (W.nseg[lane] - j >= (uint32_t)chunk) {
+                // one lane left for many segments: solo tasks from here
+                if (j > tj0) close(j, W.cur, tinit ? nullptr : &tck);
+                for (uint32_t jj = j; jj < W.max_nseg; jj++) {
+                    if ((jj - j) % chunk == 0) emit_solo(W, lane, jj, chunk, o);
+                    if (!W.step(jj)) return 0;
+                }
+                // solo cursor ends: the next solo's start, the last = slice end
+                for (size_t q = 0; q < o.solo.size(); q++)
+                    o.solo[q].cur1 = q + 1 < o.solo.size() ? o.solo[q + 1].cur0 : (uint32_t)W.nw;
+                return W.cur == W.nw ? 1 : 0;
+            }
+        }
+        const uint64_t cur_j = W.cur;
+        snap.clear();
+        if (j > 0) W.push_ck(snap, amask);
+        if (!W.step(j)) return 0;
+        if (!fits(W.cur)) {
+            if (j == tj0) return -1;
+            close(j, cur_j, tinit ? nullptr : &tck);
+            tj0 = j;
+            tcur0 = cur_j;
+            tmask = amask;
+            tinit = false;
+            tck = snap;
+            if (!fits(W.cur)) return -1;
+        }
     }
-    for (size_t q = 0; q < ends.size(); q++) *ends[q] = q + 1 < ends.size() ? starts[q + 1] : (uint32_t)nw;
-    (void)ntasks;
-    return cur == nw;
+    if (W.cur != W.nw) return 0;
+    close(W.max_nseg, W.cur, tinit ? nullptr : &tck);
+    return 1;
 }
 
 }  // namespace
 
 int build_long_index(const dtans_container_view *c, int seg_threshold, uint64_t max_words, int chunk,
-                     LongIndex &out)
+                     uint64_t stage_words, LongIndex &out)
 {
     out = LongIndex();
     const int64_t nsl = c->nslices;
@@ -242,43 +344,71 @@ int build_long_index(const dtans_container_view *c, int seg_threshold, uint64_t 
         const int rec = c->precision == 8 ? 16 : 12;
         for (int j = 0; j < kK; j++) memcpy(&dsym[j], c->tables + (size_t)j * rec + (c->precision == 8 ? 8 : 4), 4);
     }
-    // partial-slot bases in slice order
-    std::vector<uint32_t> base(longs.size() + 1, 0);
-    for (size_t i = 0; i < longs.size(); i++) {
-        const int64_t s = longs[i];
-        const int64_t row0 = s * kSlice, row1 = std::min<int64_t>(row0 + kSlice, c->rows);
-        uint32_t mx = 0;
-        for (int64_t r = row0; r < row1; r++) mx = std::max(mx, c->row_symbols[r]);
-        base[i + 1] = base[i] + ((mx + 7) / 8 + chunk - 1) / chunk;
-    }
+    std::vector<SliceOut> outs(longs.size());
     const int nt = std::max(1, std::min<int>((int)std::thread::hardware_concurrency(), (int)longs.size()));
-    std::vector<std::vector<uint32_t>> pools(nt);
-    std::vector<std::vector<LongTask>> tasks(nt);
-    std::vector<std::vector<SoloTask>> solos(nt);
     std::atomic<size_t> next{0};
     std::atomic<int> bad{0};
     std::vector<std::thread> th;
     for (int t = 0; t < nt; t++)
-        th.emplace_back([&, t]() {
+        th.emplace_back([&]() {
             for (;;) {
                 const size_t i = next.fetch_add(1);
                 if (i >= longs.size()) break;
-                if (!walk_slice(c, T, dsym.data(), longs[i], chunk, pools[t], tasks[t], solos[t], base[i])) bad = 1;
+                int ok = -1;
+                if (stage_words > 0) {
+                    SliceWalk W(c, T, dsym.data(), longs[i]);
+                    ok = walk_staged(W, chunk, stage_words, outs[i]);
+                }
+                if (ok < 0) {
+                    outs[i] = SliceOut();
+                    SliceWalk W(c, T, dsym.data(), longs[i]);
+                    ok = walk_fixed(W, chunk, outs[i]) ? 1 : 0;
+                    // global-task cursor ends: the next task's start (warp
+                    // tasks precede the slice's solo tasks), the last = slice end
+                    std::vector<uint32_t *> ends;
+                    std::vector<uint32_t> starts;
+                    for (auto &tk : outs[i].tasks) {
+                        ends.push_back(&tk.cur1);
+                        starts.push_back(tk.cur0);
+                    }
+                    for (auto &tk : outs[i].solo) {
+                        ends.push_back(&tk.cur1);
+                        starts.push_back(tk.cur0);
+                    }
+                    for (size_t q = 0; q < ends.size(); q++)
+                        *ends[q] = q + 1 < ends.size() ? starts[q + 1] : (uint32_t)W.nw;
+                }
+                if (ok != 1) bad = 1;
             }
         });
     for (auto &x : th) x.join();
     if (bad) return fail(DTANS_E_CORRUPT, "long slice consumed an unexpected number of words");
-    for (int t = 0; t < nt; t++) {
-        const uint32_t off = (uint32_t)out.pool.size();
-        for (auto tk : tasks[t]) {
-            if (tk.ck != 0xFFFFFFFFu) tk.ck += off;
+    // merge in slice order: partial-slot bases and pool offsets
+    std::vector<uint32_t> base(longs.size() + 1, 0);
+    for (size_t i = 0; i < longs.size(); i++) {
+        SliceOut &o = outs[i];
+        const uint32_t s = longs[i], pb = base[i], po = (uint32_t)out.pool.size();
+        base[i + 1] = pb + o.nparts;
+        for (auto tk : o.tasks) {
+            tk.slice = s;
+            tk.part += pb;
+            if (tk.ck != 0xFFFFFFFFu) tk.ck += po;
             out.tasks.push_back(tk);
         }
-        for (auto tk : solos[t]) {
-            tk.ck += off;
+        for (auto tk : o.solo) {
+            tk.slice = s;
+            tk.part += pb;
+            tk.ck += po;
             out.solo.push_back(tk);
         }
-        out.pool.insert(out.pool.end(), pools[t].begin(), pools[t].end());
+        for (auto tk : o.staged) {
+            tk.slice = s;
+            tk.part += pb;
+            if (tk.ck != 0xFFFFFFFFu) tk.ck += po;
+            out.staged.push_back(tk);
+        }
+        out.pool.insert(out.pool.end(), o.pool.begin(), o.pool.end());
+        o = SliceOut();
     }
     // longest tasks first (LPT) so the tail of the task kernel is short
     std::stable_sort(out.tasks.begin(), out.tasks.end(),

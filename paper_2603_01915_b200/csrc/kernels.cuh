@@ -42,6 +42,14 @@
 
 #include "checkpoints.h"
 
+// Build-time switches for A/B experiments (DESIGN 5c); the defaults are the product.
+#ifndef DTANS_RECASYNC
+#define DTANS_RECASYNC 0  // 1: chunk records prefetched with cp.async a chunk ahead (banded -2.6%: off)
+#endif
+#ifndef DTANS_GMEM_CS
+#define DTANS_GMEM_CS 0  // 1: long-slice stream words via ld.global.cs.nc (R-MAT +2.5%: off)
+#endif
+
 namespace dtans {
 namespace dev {
 
@@ -53,6 +61,7 @@ constexpr int kSlots = 4096;
 constexpr int kMaxWarps = 32;  // warps per CTA of the main kernel
 constexpr int kMaxRing = 2;     // staging buffers per warp (a double-buffered ring)
 constexpr int kMaxChunk = 16;   // slices per chunk
+constexpr uint32_t kTaskK = 0xFF;  // ChunkRec k of a staged long-slice task
 constexpr uint32_t kTabBytes = 2 * kSlots * 4;
 constexpr uint32_t kDeltaInlineEsc = 0xFFFF0000u;  // inline deltas: F = 0xFFFF marks an escape
 
@@ -269,6 +278,16 @@ struct SmemSrc {
 };
 struct GmemSrc {
     const uint32_t *p;  // &stream[directory[s]]
+#if DTANS_GMEM_CS
+    // streamed words: ld.global.cs.nc (evict-first in L1 and L2, so the
+    // gathered x stays cached), no cache-policy register
+    __device__ __forceinline__ uint32_t operator()(uint32_t rel) const
+    {
+        uint32_t v;
+        asm("ld.global.cs.nc.u32 %0, [%1];" : "=r"(v) : "l"(p + rel));
+        return v;
+    }
+#else
     unsigned long long pol;  // L2 evict-first policy (streamed words)
     __device__ __forceinline__ uint32_t operator()(uint32_t rel) const
     {
@@ -276,6 +295,7 @@ struct GmemSrc {
         asm("ld.global.nc.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(p + rel), "l"(pol));
         return v;
     }
+#endif
     __device__ __forceinline__ void prepare(uint32_t) {}
 };
 
@@ -741,10 +761,27 @@ __device__ __forceinline__ void init_state(const Ctx &C, Src &src, const uint32_
 #ifndef DTANS_YSTREAM
 #define DTANS_YSTREAM 1
 #endif
+#ifndef DTANS_YCS
+#define DTANS_YCS 1
+#endif
 template <typename V> __device__ __forceinline__ V ld_stream(const V *p)
 {
-#if DTANS_YSTREAM
+#if DTANS_YSTREAM && DTANS_YCS
     return __ldcs(p);  // ld.global.cs: evict-first in L1 and L2, no policy register
+#elif DTANS_YSTREAM
+    V v;
+    if (sizeof(V) == 8) {
+        unsigned long long b;
+        asm("{\n.reg .b64 pol;\ncreatepolicy.fractional.L2::evict_first.b64 pol, 1.0;\n"
+            "ld.global.nc.L1::no_allocate.L2::cache_hint.b64 %0, [%1], pol;\n}" : "=l"(b) : "l"(p));
+        memcpy(&v, &b, 8);
+    } else {
+        uint32_t b;
+        asm("{\n.reg .b64 pol;\ncreatepolicy.fractional.L2::evict_first.b64 pol, 1.0;\n"
+            "ld.global.nc.L1::no_allocate.L2::cache_hint.b32 %0, [%1], pol;\n}" : "=r"(b) : "l"(p));
+        memcpy(&v, &b, 4);
+    }
+    return v;
 #else
     return __ldg(p);
 #endif
@@ -834,6 +871,68 @@ __device__ __forceinline__ void cp_async16(uint32_t dst, const void *src)
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
+// A staged long-slice task (api.cu assemble_task): segments [j0, j1) of a
+// long slice from its staged blob
+//   [slice, j0, j1, part, nwin, max_nseg, min_nseg | np << 16 | last << 24, ckw]
+//   [32 row_symbols][resume record: mask, 0, 6 words per active lane][nwin words]
+// (checkpoints.cpp walk_staged).  Single-task slices write y' here; the
+// others leave a per-lane partial sum for dtans_finalize_kernel.
+template <typename V, bool kDecode, bool kHasY, bool kDIn, bool kScaled>
+__device__ __forceinline__ void decode_staged_task(const KernelArgs &a, const Ctx &C, const V *__restrict__ x,
+                                                   const uint32_t buf, const int lane, const V scale, double &wsum)
+{
+    using T = ValueTraits<V>;
+    const uint4 h0 = ld_shared_v4(buf);
+    const uint4 h1 = ld_shared_v4(buf + 16u);
+    const uint32_t slice = h0.x, j0 = h0.y, j1 = h0.z, part = h0.w;
+    const uint32_t nwin = h1.x, max_nseg = h1.y;
+    const uint32_t min_nseg = h1.z & 0xFFFFu, np = (h1.z >> 16) & 0xFFu;
+    const bool last = (h1.z >> 24) != 0u;
+    const uint32_t ckw = h1.w;
+    const uint32_t n = sh32(buf + 32u + (uint32_t)lane * 4u);
+    const uint32_t row = slice * kSliceRows + (uint32_t)lane;
+    const bool inrow = row < (uint32_t)a.rows;
+    SmemSrc src{buf + (40u + ckw) * 4u};
+    LaneState<V> st;
+    st.out_pos = 0;
+    if (ckw == 0u) {
+        init_state<V>(C, src, n, st);
+    } else {
+        const uint32_t mask = sh32(buf + 160u);
+        const bool active = (mask >> lane) & 1u;
+        const uint32_t pk = buf + 168u + 24u * (uint32_t)__popc(mask & C.lt);
+        const uint2 q0 = ld_shared_v2(pk), q1 = ld_shared_v2(pk + 8u), q2 = ld_shared_v2(pk + 16u);
+        st.w0 = active ? q0.x : 0u;
+        st.w1 = active ? q0.y : 0u;
+        st.w2 = active ? q1.x : 0u;
+        st.d = active ? q1.y : 0u;
+        st.r = active ? q2.x : 1u;
+        st.col = active ? q2.y : 0u;
+        st.cur = 0u;
+        st.acc = V(0);
+    }
+    // decoding: every segment before j0 of an active lane was full (4 pairs)
+    if (kDecode && inrow) st.out_pos = __ldg(a.row_start + row) + 4ll * j0;
+    const bool ok = decode_range<V, kDecode, kDIn>(a, C, x, src, nwin, n, max_nseg, min_nseg, np, j0, j1, st, lane);
+    report(a, C, ok, st.cur, nwin, last ? n : 0u, st.col, lane);
+    if (kDecode) return;
+    if (last && j0 == 0u) {
+        // the slice is this single task: y' = acc + y directly
+        if (inrow) {
+            const uint32_t orow = a.row_map != nullptr ? __ldg(a.row_map + row) : row;
+            V res = st.acc;
+            if (kHasY) res = T::add(res, ld_stream(reinterpret_cast<const V *>(a.y) + orow));
+            if (kScaled) {
+                res = T::mul(res, scale);
+                wsum = __dadd_rn(wsum, __dmul_rn((double)res, (double)res));
+            }
+            st_stream(reinterpret_cast<V *>(a.out) + orow, res);
+        }
+    } else {
+        reinterpret_cast<V *>(a.partials)[(size_t)part * 32 + lane] = st.acc;
+    }
+}
+
 // Chunk staging (lane 0): one cp.async.bulk of the chunk's blob completing
 // on the buffer's mbarrier.  The previous contents were consumed by this
 // warp's LDS before the __syncwarp that precedes the call (the same WAR
@@ -865,7 +964,9 @@ struct WarpCtl {
 // Persistent kernel, one CTA of 32 warps per SM: tables -> shared memory once,
 // then every warp walks chunks (static stride or atomic tickets) through its
 // TMA ring.
-template <typename V, bool kDecode, bool kHasY, bool kDIn, bool kScaled = false>
+// kTasks: the chunk list also holds staged long-slice tasks (a separate
+// instantiation, so matrices without long slices do not pay its registers).
+template <typename V, bool kDecode, bool kHasY, bool kDIn, bool kScaled = false, bool kTasks = false>
 __global__ void __launch_bounds__(kMaxWarps * 32, 1) dtans_kernel(const KernelArgs a)
 {
     constexpr int kWarps = kMaxWarps;
@@ -918,7 +1019,13 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) dtans_kernel(const KernelAr
         }
         const uint32_t c = claim();
         ctl->pend_ok = c < a.chunk_hi;
-        if (c < a.chunk_hi) cp_async16(ctl_sh, a.chunks + c);
+        if (c < a.chunk_hi) {
+#if DTANS_RECASYNC
+            cp_async16(ctl_sh, a.chunks + c);
+#else
+            ctl->pend = a.chunks[c];
+#endif
+        }
         ctl->pend_c = claim();
     }
     __syncwarp();
@@ -928,6 +1035,10 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) dtans_kernel(const KernelAr
         const uint2 md = ld_shared_v2(metas + 8u * b);
         const uint32_t s0 = md.x, k = md.y;
         if (k == 0) break;  // uniform: this warp's chunks are exhausted
+        if (kTasks && k == kTaskK) {  // uniform: a staged long-slice task
+            decode_staged_task<V, kDecode, kHasY, kDIn, kScaled>(a, C, x, bufs + b * (uint32_t)a.bufb, lane, scale,
+                                                                  wsum);
+        } else {
         // the chunk's addresses live in the warp's control block and are
         // re-read per slice (one LDS.128) instead of occupying registers
         // across the decode
@@ -949,13 +1060,22 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) dtans_kernel(const KernelAr
                                                             (cs.w + i) * kSliceRows + (uint32_t)lane, lane, scale, wsum);
             dcur = dnext;
         }
+        }
         __syncwarp();
         if (lane == 0) {
+#if DTANS_RECASYNC
             cp_async_wait_all();  // the pending record (issued a chunk ago)
+#endif
             stage_chunk(a, ctl->pend_ok != 0u, ctl->pend, bars + 8u * b, metas + 8u * b, bufs + b * (uint32_t)a.bufb);
             const uint32_t c = ctl->pend_c;
             ctl->pend_ok = c < a.chunk_hi;
-            if (c < a.chunk_hi) cp_async16(ctl_sh, a.chunks + c);
+            if (c < a.chunk_hi) {
+#if DTANS_RECASYNC
+                cp_async16(ctl_sh, a.chunks + c);
+#else
+                ctl->pend = a.chunks[c];
+#endif
+            }
             ctl->pend_c = claim();
         }
         __syncwarp();
@@ -999,7 +1119,11 @@ __global__ void __launch_bounds__(kTaskWarps * 32, 1024 / (kTaskWarps * 32)) dta
         const uint32_t n = inrow ? __ldg(a.row_symbols + row) : 0u;
         uint32_t max_nseg, min_nseg, np;
         slice_shape(C, n, max_nseg, min_nseg, np);
+#if DTANS_GMEM_CS
+        GmemSrc src{a.stream + __ldg(a.directory + tk.slice)};
+#else
         GmemSrc src{a.stream + __ldg(a.directory + tk.slice), pol};
+#endif
         {
             // pull the task's stream words into L1 up front (coalesced line
             // prefetches) so the loads on the serial per-segment chain hit L1

@@ -67,15 +67,21 @@ def long_slice_rows(row_start, rows):
     return np.repeat(long_slice, 32)[:rows]
 
 
-def check_spmv(out, ref, m, x, y):
+def check_spmv(out, ref, m, x, y, c=None):
     """Parity policy (north star / SURVEY 8c): bitwise for rows decoded in
-    lockstep order; for long-slice rows |out-ref| <= tol*(sum|a x| + |y|),
-    tol 1e-12 (f64) / 1e-5 (f32); NaN == NaN."""
+    lockstep order; for rows whose slice was split into several tasks
+    |out-ref| <= tol*(sum|a x| + |y|), tol 1e-12 (f64) / 1e-5 (f32);
+    NaN == NaN.  With the container ``c`` (rows in the order of ``out``) the
+    split rows are the device plan's (dtans_split_slices); otherwise every
+    slice longer than one 16-segment task counts as split."""
     out = np.asarray(out)
     ref = np.asarray(ref)
     if out.shape != ref.shape or out.dtype != ref.dtype:
         return False
-    lr = long_slice_rows(m.row_start, m.rows)
+    if c is not None:
+        lr = c.device(0).split_rows(m.rows) | long_slice_rows(m.row_start, m.rows)
+    else:
+        lr = long_slice_rows(m.row_start, m.rows)
     if not same_bits_or_nan(out[~lr], ref[~lr]):
         return False
     if not lr.any():

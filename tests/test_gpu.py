@@ -23,7 +23,7 @@ def test_spmv_bitwise_reference(name):
     rec = G.load(name)
     c = P.encode_matrix(G.matrix(rec), **G.encode_kwargs(rec))
     out = P.spmv(c, rec["x"], rec["y"])
-    assert G.check_spmv(out, rec["spmv"], G.matrix(rec), rec["x"], rec["y"])
+    assert G.check_spmv(out, rec["spmv"], G.matrix(rec), rec["x"], rec["y"], c=c)
 
 
 @pytest.mark.parametrize("name", G.names())
@@ -41,7 +41,7 @@ def test_spmv_from_reference_bytes(name):
     rec = G.load(name)
     c = P.deserialize(rec["container"].tobytes())
     out = P.spmv(c, rec["x"], rec["y"])
-    assert G.check_spmv(out, rec["spmv"], G.matrix(rec), rec["x"], rec["y"])
+    assert G.check_spmv(out, rec["spmv"], G.matrix(rec), rec["x"], rec["y"], c=c)
 
 
 def test_corrupt_directory_raises():
@@ -85,7 +85,7 @@ def test_larger_matrices_vs_oracle(gen):
     assert P.decode_matrix(c) == m
     out = P.spmv(c, x, y)
     ref = O.spmv(O.parse(P.serialize(c)), x, y, threads=8)
-    assert G.check_spmv(out, ref, m, x, y)
+    assert G.check_spmv(out, ref, m, x, y, c=c)
 
 
 @pytest.mark.parametrize("world", [2, 3])
@@ -103,7 +103,8 @@ def test_sharded_spmv_on_gpu_equals_full(world):
         if sc.rows:
             sc.device(0).check()
             o = out.cpu().numpy()
-            lr = G.long_slice_rows(m.row_start[r0:r1 + 1] - m.row_start[r0], r1 - r0)
+            lr = G.long_slice_rows(m.row_start[r0:r1 + 1] - m.row_start[r0], r1 - r0) | \
+                sc.device(0).split_rows(r1 - r0) | c.device(0).split_rows(m.rows)[r0:r1]
             assert G.same_bits_or_nan(o[~lr], full[r0:r1][~lr])
             assert np.allclose(o[lr], full[r0:r1][lr], rtol=1e-5, atol=1e-4)
 
@@ -154,7 +155,7 @@ def test_row_reordered_rmat(window):
     ref[perm.astype(np.int64)] = ref_p
     exp_p = np.empty_like(out)
     exp_p = out[perm.astype(np.int64)]
-    assert G.check_spmv(exp_p, ref_p, pm, x, y[perm.astype(np.int64)])
+    assert G.check_spmv(exp_p, ref_p, pm, x, y[perm.astype(np.int64)], c=c)
 
 
 @pytest.mark.parametrize("dtype", [np.float64, np.float32])
@@ -192,7 +193,7 @@ def test_symmetric_reordered_rmat():
     out = P.spmv(c, x, y)
     p64 = perm.astype(np.int64)
     ref_p = O.spmv(O.parse(P.serialize(c)), x[p64], y[p64], threads=8)
-    assert G.check_spmv(out[p64], ref_p, pm, x[p64], y[p64])
+    assert G.check_spmv(out[p64], ref_p, pm, x[p64], y[p64], c=c)
     # and through the device-tensor path
     dev = c.device(0)
     o2 = dev.spmv(torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda())

@@ -86,7 +86,7 @@ def test_two_gloo_ranks_on_one_gpu(tmp_path, dtype_name):
         ms = P.CsrMatrix(r1 - r0, m.cols, rs, m.col_idx[m.row_start[r0]:m.row_start[r1]],
                          m.values[m.row_start[r0]:m.row_start[r1]])
         assert sub.rows == r1 - r0
-        assert G.check_spmv(out, ref, ms, x, y[r0:r1])
+        assert G.check_spmv(out, ref, ms, x, y[r0:r1], c=sub)
     mb = synth.banded(20000, 32, positive=True, seed=3)
     xr, lr = D.reference_power_iteration(mb, np.full(mb.cols, 1.0 / np.sqrt(mb.cols)), 25)
     tol = 1e-12 if dtype == np.float64 else 1e-5

@@ -73,7 +73,7 @@ def test_goldens_multichunk(name, kchunk, monkeypatch):
     c = _fresh(P.encode_matrix(m, **G.encode_kwargs(rec)))
     out = P.spmv(c, rec["x"], rec["y"])
     _assert_multichunk(c.device(0), c, kchunk)
-    assert G.check_spmv(out, rec["spmv"], m, rec["x"], rec["y"])
+    assert G.check_spmv(out, rec["spmv"], m, rec["x"], rec["y"], c=c)
     vdt = np.float64 if c.precision == 8 else np.float32
     assert P.decode_matrix(c) == P.CsrMatrix(m.rows, m.cols, m.row_start, m.col_idx, m.values.astype(vdt))
 
@@ -102,11 +102,11 @@ def test_mid_matrices_multichunk(gen, kchunk, monkeypatch):
     yt = torch.from_numpy(np.ascontiguousarray(y, V)).cuda()
     out = dc.spmv(xt, yt).cpu().numpy()
     dc.check()
-    assert G.check_spmv(out, ref, m, x, y)
+    assert G.check_spmv(out, ref, m, x, y, c=c)
     ref0 = O.spmv(oc, x, np.zeros_like(y), threads=8)
     out0 = dc.spmv(xt, None).cpu().numpy()
     dc.check()
-    assert G.check_spmv(out0, ref0, m, x, np.zeros_like(y))
+    assert G.check_spmv(out0, ref0, m, x, np.zeros_like(y), c=c)
     # scaled: out = (A x) * (1 / sqrt(q)), sum(out^2) accumulated
     q = 7.25
     S = torch.tensor([q, 0.0, 3.0], dtype=torch.float64, device="cuda")
@@ -156,7 +156,7 @@ def test_clear_row_map_keeps_col_map():
     out = dc.spmv(torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda()).cpu().numpy()
     dc.check()
     ref = O.spmv(O.parse(P.serialize(c)), x[p64], y, threads=8)
-    assert G.check_spmv(out, ref, pm, x[p64], y)
+    assert G.check_spmv(out, ref, pm, x[p64], y, c=c)
     dc.close()
 
 
@@ -206,6 +206,6 @@ def test_streamed_upload_from_mmapped_file(gen, tmp_path, monkeypatch):
     assert plan["upload_batches"] >= 4, plan
     out = P.spmv(c, x, y)
     ref = O.spmv(O.parse(P.serialize(c0)), x, y, threads=8)
-    assert G.check_spmv(out, ref, m, x, y)
+    assert G.check_spmv(out, ref, m, x, y, c=c)
     assert P.decode_matrix(c) == P.CsrMatrix(m.rows, m.cols, m.row_start, m.col_idx,
                                              m.values.astype(c.value_dtype))
