@@ -232,7 +232,8 @@ typedef struct {
     int32_t bufb, nring;      /* staging buffer bytes, buffers per warp */
     int64_t upload_bytes;     /* bytes streamed through the pinned upload buffers */
     int64_t upload_batches;   /* cudaMemcpyAsync batches of the upload */
-    int64_t nstaged;          /* long-slice tasks the main kernel decodes from shared memory */
+    int64_t pend;             /* 1: the main kernel defers the last full segment's products past a
+                                 one-pair final segment's gathers (chosen per matrix) */
 } dtans_plan_t;
 int dtans_plan(const dtans_dev *h, dtans_plan_t *out);
 

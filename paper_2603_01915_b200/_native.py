@@ -74,7 +74,7 @@ class Plan(ctypes.Structure):
         ("dynamic", ctypes.c_int32), ("dinline", ctypes.c_int32),
         ("bufb", ctypes.c_int32), ("nring", ctypes.c_int32),
         ("upload_bytes", ctypes.c_int64), ("upload_batches", ctypes.c_int64),
-        ("nstaged", ctypes.c_int64),
+        ("pend", ctypes.c_int64),
     ]
 
 
@@ -119,8 +119,9 @@ def lib() -> ctypes.CDLL:
     L.dtans_launch_count.argtypes = [vp]
     L.dtans_launch_count.restype = i64
     L.dtans_plan.argtypes = [vp, ctypes.POINTER(Plan)]
-    L.dtans_split_slices.restype = ctypes.c_int64
-    L.dtans_split_slices.argtypes = [vp, vp, ctypes.c_int64]
+    if hasattr(L, "dtans_split_slices"):  # absent from older builds loaded via DTANS_LIB (A/B runs)
+        L.dtans_split_slices.restype = ctypes.c_int64
+        L.dtans_split_slices.argtypes = [vp, vp, ctypes.c_int64]
     _lib = L
     return L
 

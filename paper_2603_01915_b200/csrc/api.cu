@@ -38,7 +38,7 @@ struct dtans_dev {
     int ctas = 0, threads = 1024, smem = 0;
     int64_t launches = 0;
     int64_t staged_slices = 0;  // slices whose stream fits a ring buffer
-    int64_t nstaged = 0;        // long-slice tasks decoded by the main kernel
+    bool pend = false;          // main kernel instantiation with pending products (kernels.cuh kPend)
     std::vector<uint32_t> split_slices;  // slices whose rows sum several task partials
     size_t upload_staged_bytes = 0;  // bytes streamed through the pinned upload buffers
     int64_t upload_batches = 0;
@@ -257,8 +257,8 @@ uint64_t chunk_words(const uint64_t *dir, int64_t s0, int64_t k)
 }
 uint64_t chunk_bytes(const uint64_t *dir, int64_t s0, int64_t k) { return 4 * chunk_words(dir, s0, k); }
 
-// Dispatch on the delta-dictionary mode and on staged tasks: (spmv, y-less
-// spmv, decode, scaled y-less spmv).
+// Dispatch on the delta-dictionary mode and on the pending-products
+// instantiation: (spmv, y-less spmv, decode, scaled y-less spmv).
 template <typename V, bool kT, class F>
 int with_kernel_t(bool dinline, F &&f)
 {
@@ -269,9 +269,9 @@ int with_kernel_t(bool dinline, F &&f)
              dev::dtans_kernel<V, true, false, false, false, kT>, dev::dtans_kernel<V, false, false, false, true, kT>);
 }
 template <typename V, class F>
-int with_kernel(bool dinline, bool tasks, F &&f)
+int with_kernel(bool dinline, bool pend, F &&f)
 {
-    return tasks ? with_kernel_t<V, true>(dinline, f) : with_kernel_t<V, false>(dinline, f);
+    return pend ? with_kernel_t<V, true>(dinline, f) : with_kernel_t<V, false>(dinline, f);
 }
 
 template <typename V, class F>
@@ -345,7 +345,7 @@ int configure(dtans_dev *h, const TableBlock &tb, const SmemPlan &sp)
     h->smem = sp.total;
     h->ctas = (int)std::max<int64_t>(1, std::min<int64_t>(sms, ((int64_t)h->chunks.size() + dev::kMaxWarps - 1) / dev::kMaxWarps));
     int per_sm = 0;
-    int rc = with_kernel<V>(tb.dinline, h->nstaged > 0, [&](auto kspmv, auto kspmv0, auto kdec, auto kscaled) -> int {
+    int rc = with_kernel<V>(tb.dinline, h->pend, [&](auto kspmv, auto kspmv0, auto kdec, auto kscaled) -> int {
         CK(cudaFuncSetAttribute(kscaled, cudaFuncAttributeMaxDynamicSharedMemorySize, h->smem), "cudaFuncSetAttribute");
         CK(cudaFuncSetAttribute(kspmv, cudaFuncAttributeMaxDynamicSharedMemorySize, h->smem), "cudaFuncSetAttribute");
         CK(cudaFuncSetAttribute(kspmv0, cudaFuncAttributeMaxDynamicSharedMemorySize, h->smem), "cudaFuncSetAttribute");
@@ -400,7 +400,7 @@ int launch(dtans_dev *h, const V *x, const V *y, V *out, const int64_t *row_star
     a.sumsq_out = sumsq_out;
     a.sumsq_zero = sumsq_zero;
     if (nch > 0) {
-        with_kernel<V>(h->dinline, h->nstaged > 0, [&](auto kspmv, auto kspmv0, auto kdec, auto kscaled) -> int {
+        with_kernel<V>(h->dinline, h->pend, [&](auto kspmv, auto kspmv0, auto kdec, auto kscaled) -> int {
             if (scaled)
                 kscaled<<<ctas, h->threads, h->smem, st>>>(a);
             else if (decode_only)
@@ -483,57 +483,6 @@ void assemble_chunk(const dtans_container_view *c, const dev::ChunkRec &r, bool 
     const uint64_t nw = c->directory[s0 + k] - base;
     memcpy(p, c->stream + base, sizeof(uint32_t) * (size_t)nw);
     for (uint64_t i = nw; i < ((nw + 3) & ~3ull); i++) p[i] = 0u;
-}
-
-// Blob of a staged long-slice task (kernels.cuh decode_staged_task):
-//   [8 header words][32 row_symbols][resume record {mask, 0, 6 words per
-//   active lane}, padded to 4][window words, padded to 4]
-// header: slice, j0, j1, part, window words, max_nseg, min_nseg | np << 16 |
-// last << 24, resume-record words (0: start from the init events).
-uint64_t staged_ck_words(const LongIndex &li, const StagedTask &t)
-{
-    if (t.ck == 0xFFFFFFFFu) return 0;
-    return (2 + 6 * (uint64_t)__builtin_popcount(li.pool[t.ck]) + 3) & ~3ull;
-}
-uint64_t staged_words(const LongIndex &li, const StagedTask &t)
-{
-    return 8 + 32 + staged_ck_words(li, t) + ((uint64_t)(t.cur1 - t.cur0 + 3) & ~3ull);
-}
-void assemble_task(const dtans_container_view *c, const LongIndex &li, const StagedTask &t, bool pads_ok, uint32_t *p)
-{
-    const int64_t r0 = (int64_t)t.slice * kSlice, r1 = std::min<int64_t>(r0 + kSlice, c->rows);
-    uint32_t maxn = 0, minseg = 0xFFFFFFFFu;
-    for (int64_t l = 0; l < kSlice; l++) {
-        const uint32_t n = r0 + l < r1 ? c->row_symbols[r0 + l] : 0u;
-        maxn = std::max(maxn, n);
-        minseg = std::min(minseg, (n + 7u) / 8u);
-    }
-    const uint32_t mseg = (maxn + 7u) / 8u;
-    const uint32_t np = pads_ok && mseg > 0 ? (maxn - 8u * (mseg - 1u)) / 2u : 4u;
-    const uint32_t ckw = (uint32_t)staged_ck_words(li, t);
-    const uint32_t nwin = t.cur1 - t.cur0;
-    p[0] = t.slice;
-    p[1] = t.j0;
-    p[2] = t.j1;
-    p[3] = t.part;
-    p[4] = nwin;
-    p[5] = mseg;
-    p[6] = minseg | np << 16 | (t.last ? 1u : 0u) << 24;
-    p[7] = ckw;
-    for (int64_t l = 0; l < kSlice; l++) p[8 + l] = r0 + l < r1 ? c->row_symbols[r0 + l] : 0u;
-    p += 40;
-    if (ckw) {
-        // {mask, 0 (8-byte alignment of the lane records), lanes' records}
-        const uint32_t *ck = li.pool.data() + t.ck;
-        const uint32_t len = 6 * (uint32_t)__builtin_popcount(ck[0]);
-        p[0] = ck[0];
-        p[1] = 0u;
-        memcpy(p + 2, ck + 1, 4 * (size_t)len);
-        for (uint32_t i = 2 + len; i < ckw; i++) p[i] = 0u;
-        p += ckw;
-    }
-    memcpy(p, c->stream + c->directory[t.slice] + t.cur0, 4 * (size_t)nwin);
-    for (uint32_t i = nwin; i < ((nwin + 3) & ~3u); i++) p[i] = 0u;
 }
 
 // Host->device copies through two pinned staging buffers on one stream:
@@ -676,12 +625,7 @@ extern "C" int dtans_upload(const dtans_container_view *c, int device, dtans_dev
     LongIndex li;
     {
         const uint64_t max_words = (uint64_t)(sp.bufb - 16 - 128) / 4;
-        // staged tasks (DTANS_STAGED, default on): long slices are cut into
-        // tasks whose blob fits one staging buffer and go through the main
-        // kernel's TMA ring; 0 = global-memory task kernel only
-        const char *es = getenv("DTANS_STAGED");
-        const uint64_t stage_words = (es && atoi(es) == 0) ? 0 : (uint64_t)sp.bufb / 4;
-        const int rc0 = build_long_index(c, long_seg, max_words, std::max(1, chunk), stage_words, li);
+        const int rc0 = build_long_index(c, long_seg, max_words, std::max(1, chunk), li);
         if (rc0) {
             delete h;
             return rc0;
@@ -711,7 +655,7 @@ extern "C" int dtans_upload(const dtans_container_view *c, int device, dtans_dev
         }
         mean /= (double)std::max<int64_t>(nsl, 1);
         const char *ed = getenv("DTANS_DYNAMIC");
-        const bool dyn = ed ? atoi(ed) != 0 : (mx > 4.0 * std::max(mean, 1.0) || !li.staged.empty());
+        const bool dyn = ed ? atoi(ed) != 0 : (mx > 4.0 * std::max(mean, 1.0));
         h->base.dynamic = dyn ? 1 : 0;
         bool sorted = true;
         for (int64_t s = 1; s < nsl && sorted; s++)
@@ -726,20 +670,7 @@ extern "C" int dtans_upload(const dtans_container_view *c, int device, dtans_dev
             h->chunks.push_back(dev::ChunkRec{blob_words, (uint32_t)s0, (uint32_t)k | (uint32_t)w << 8});
             blob_words += w;
         };
-        // staged long-slice tasks first, largest windows first (LPT)
-        {
-            std::vector<uint32_t> order(li.staged.size());
-            for (size_t i = 0; i < order.size(); i++) order[i] = (uint32_t)i;
-            std::stable_sort(order.begin(), order.end(), [&](uint32_t p, uint32_t q) {
-                return li.staged[p].cur1 - li.staged[p].cur0 > li.staged[q].cur1 - li.staged[q].cur0;
-            });
-            for (uint32_t i : order) {
-                const uint64_t w = staged_words(li, li.staged[i]);
-                h->chunks.push_back(dev::ChunkRec{blob_words, i, dev::kTaskK | (uint32_t)w << 8});
-                blob_words += w;
-            }
-            h->nstaged = (int64_t)li.staged.size();
-        }
+
         if (dyn && !sorted) {
             // skewed, unsorted: single-slice chunks, longest first
             std::vector<uint32_t> order;
@@ -763,6 +694,25 @@ extern "C" int dtans_upload(const dtans_container_view *c, int device, dtans_dev
             }
         }
         h->blob_words = blob_words;
+        // the pending-products instantiation pays off where most staged
+        // slices are hot up to a one-pair final segment (kernels.cuh
+        // decode_range kPend, e.g. the 5-point Laplacian); elsewhere its
+        // extra registers only cost (DTANS_PEND=0/1 forces it)
+        int64_t staged = 0, pendable = 0;
+        for (int64_t s = 0; s < nsl; s++) {
+            if (is_long[s]) continue;
+            staged++;
+            uint32_t maxn = 0, minseg = 0xFFFFFFFFu;
+            for (int64_t i = s * kSlice; i < (s + 1) * kSlice; i++) {
+                const uint32_t n = i < c->rows ? c->row_symbols[i] : 0u;
+                maxn = std::max(maxn, n);
+                minseg = std::min(minseg, (n + 7u) / 8u);
+            }
+            const uint32_t mseg = (maxn + 7u) / 8u;
+            if (pads_ok && mseg >= 2 && minseg == mseg && maxn - 8u * (mseg - 1u) <= 2u) pendable++;
+        }
+        const char *ep = getenv("DTANS_PEND");
+        h->pend = ep ? atoi(ep) != 0 : (staged > 0 && 2 * pendable >= staged);
     }
 
     // one allocation: [table image][chunk blobs][err][chunk records]
@@ -838,10 +788,7 @@ extern "C" int dtans_upload(const dtans_container_view *c, int device, dtans_dev
             parallel_for(qe - q, [&](size_t lo, size_t hi) {
                 for (size_t i = lo; i < hi; i++) {
                     const dev::ChunkRec &r = h->chunks[q + i];
-                    if ((r.kw & 0xFF) == dev::kTaskK)
-                        assemble_task(c, li, li.staged[r.s0], pads_ok, dst + (r.off - off0));
-                    else
-                        assemble_chunk(c, r, pads_ok, dst + (r.off - off0));
+                    assemble_chunk(c, r, pads_ok, dst + (r.off - off0));
                 }
             });
             if (!up.submit(h->d_blob + off0, words * 4)) rc = cuda_fail(up.err, "upload chunk blobs");
@@ -1011,7 +958,7 @@ extern "C" int dtans_plan(const dtans_dev *h, dtans_plan_t *out)
     out->nring = h->base.nring;
     out->upload_bytes = (int64_t)h->upload_staged_bytes;
     out->upload_batches = h->upload_batches;
-    out->nstaged = h->nstaged;
+    out->pend = h->pend ? 1 : 0;
     return DTANS_OK;
 }
 

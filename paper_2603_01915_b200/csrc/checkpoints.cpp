@@ -196,7 +196,6 @@ struct SliceWalk {
 struct SliceOut {
     std::vector<LongTask> tasks;
     std::vector<SoloTask> solo;
-    std::vector<StagedTask> staged;
     std::vector<uint32_t> pool;  // slice-local offsets
     uint32_t nparts = 0;
 };
@@ -246,84 +245,10 @@ bool walk_fixed(SliceWalk &W, int chunk, SliceOut &o)
     return W.cur == W.nw;
 }
 
-// Words a staged task's blob needs besides its window (api.cu
-// staged_blob_words): header, the 32 row_symbols, the resume record.
-uint64_t staged_fixed_words(uint32_t mask, bool from_init)
-{
-    return 8 + 32 + (from_init ? 0 : ((2 + 6 * (uint64_t)__builtin_popcount(mask) + 3) & ~3ull));
-}
-
-// Staged tasks cut where the blob would overflow stage_words.  Returns 1 on
-// success, 0 on a corrupt slice, -1 if one segment alone does not fit (the
-// caller falls back to walk_fixed).
-int walk_staged(SliceWalk &W, int chunk, uint64_t stage_words, SliceOut &o)
-{
-    if (!W.init()) return 0;
-    uint32_t tj0 = 0, tmask = 0;
-    uint64_t tcur0 = 0;
-    bool tinit = true;
-    std::vector<uint32_t> snap;  // resume record at the current segment start
-    auto fits = [&](uint64_t cur1) {
-        return staged_fixed_words(tmask, tinit) + ((cur1 - tcur0 + 3) & ~3ull) <= stage_words;
-    };
-    auto close = [&](uint32_t j1, uint64_t cur1, const std::vector<uint32_t> *ck) {
-        StagedTask t;
-        t.slice = 0;
-        t.j0 = tj0;
-        t.j1 = j1;
-        t.part = o.nparts++;
-        t.cur0 = (uint32_t)tcur0;
-        t.cur1 = (uint32_t)cur1;
-        t.last = j1 == W.max_nseg;
-        t.ck = 0xFFFFFFFFu;
-        if (ck) {
-            t.ck = (uint32_t)o.pool.size();
-            o.pool.insert(o.pool.end(), ck->begin(), ck->end());
-        }
-        o.staged.push_back(t);
-    };
-    std::vector<uint32_t> tck;  // resume record of the open task
-    for (uint32_t j = 0; j < W.max_nseg; j++) {
-        const uint32_t amask = W.active_mask(j);
-        if (j > 0 && __builtin_popcount(amask) == 1) {
-            const int lane = __builtin_ctz(amask);
-            if (W.nseg[lane] - j >= (uint32_t)chunk) {
-                // one lane left for many segments: solo tasks from here
-                if (j > tj0) close(j, W.cur, tinit ? nullptr : &tck);
-                for (uint32_t jj = j; jj < W.max_nseg; jj++) {
-                    if ((jj - j) % chunk == 0) emit_solo(W, lane, jj, chunk, o);
-                    if (!W.step(jj)) return 0;
-                }
-                // solo cursor ends: the next solo's start, the last = slice end
-                for (size_t q = 0; q < o.solo.size(); q++)
-                    o.solo[q].cur1 = q + 1 < o.solo.size() ? o.solo[q + 1].cur0 : (uint32_t)W.nw;
-                return W.cur == W.nw ? 1 : 0;
-            }
-        }
-        const uint64_t cur_j = W.cur;
-        snap.clear();
-        if (j > 0) W.push_ck(snap, amask);
-        if (!W.step(j)) return 0;
-        if (!fits(W.cur)) {
-            if (j == tj0) return -1;
-            close(j, cur_j, tinit ? nullptr : &tck);
-            tj0 = j;
-            tcur0 = cur_j;
-            tmask = amask;
-            tinit = false;
-            tck = snap;
-            if (!fits(W.cur)) return -1;
-        }
-    }
-    if (W.cur != W.nw) return 0;
-    close(W.max_nseg, W.cur, tinit ? nullptr : &tck);
-    return 1;
-}
-
 }  // namespace
 
 int build_long_index(const dtans_container_view *c, int seg_threshold, uint64_t max_words, int chunk,
-                     uint64_t stage_words, LongIndex &out)
+                     LongIndex &out)
 {
     out = LongIndex();
     const int64_t nsl = c->nslices;
@@ -354,13 +279,8 @@ int build_long_index(const dtans_container_view *c, int seg_threshold, uint64_t 
             for (;;) {
                 const size_t i = next.fetch_add(1);
                 if (i >= longs.size()) break;
-                int ok = -1;
-                if (stage_words > 0) {
-                    SliceWalk W(c, T, dsym.data(), longs[i]);
-                    ok = walk_staged(W, chunk, stage_words, outs[i]);
-                }
-                if (ok < 0) {
-                    outs[i] = SliceOut();
+                int ok = 0;
+                {
                     SliceWalk W(c, T, dsym.data(), longs[i]);
                     ok = walk_fixed(W, chunk, outs[i]) ? 1 : 0;
                     // global-task cursor ends: the next task's start (warp
@@ -400,12 +320,6 @@ int build_long_index(const dtans_container_view *c, int seg_threshold, uint64_t 
             tk.part += pb;
             tk.ck += po;
             out.solo.push_back(tk);
-        }
-        for (auto tk : o.staged) {
-            tk.slice = s;
-            tk.part += pb;
-            if (tk.ck != 0xFFFFFFFFu) tk.ck += po;
-            out.staged.push_back(tk);
         }
         out.pool.insert(out.pool.end(), o.pool.begin(), o.pool.end());
         o = SliceOut();

@@ -24,16 +24,6 @@ struct SoloTask {
     uint32_t part, cur0, cur1, ck;
 };
 
-// A staged task: segments [j0, j1) of a long slice whose words [cur0,
-// cur1) fit one staging buffer together with the slice's row_symbols and the
-// resume state, so the main kernel decodes it from shared memory like a
-// chunk (one TMA bulk copy).  ck indexes {mask, per active lane w0, w1, w2,
-// d, r, col} in the pool, or 0xFFFFFFFF (start from the init events).
-struct StagedTask {
-    uint32_t slice, j0, j1, part;
-    uint32_t cur0, cur1, ck, last;
-};
-
 struct LongSlice {
     uint32_t slice, part_base, nparts, pad;
 };
@@ -41,7 +31,6 @@ struct LongSlice {
 struct LongIndex {
     std::vector<LongTask> tasks;     // global-memory warp tasks (task kernel)
     std::vector<SoloTask> solo;      // single-lane tasks (solo kernel)
-    std::vector<StagedTask> staged;  // shared-memory tasks (main kernel)
     std::vector<uint32_t> pool;
     std::vector<LongSlice> slices;
     uint32_t nparts = 0;
@@ -49,13 +38,10 @@ struct LongIndex {
 
 // Slices whose longest row has more than seg_threshold segments, or whose
 // 16-byte aligned stream window exceeds max_words (does not fit a staging
-// buffer), are long.  With stage_words > 0 a long slice is cut into staged
-// tasks whose resume state + words fit stage_words (a new task starts at the
-// segment where the window would overflow); a slice with a segment larger
-// than that falls back to global-memory tasks of `chunk` segments.  Once a
-// single lane is left at a task boundary, its remaining segments become solo
-// tasks of `chunk` segments.
+// buffer), are long: they are split into warp tasks of `chunk` segments, and
+// once a single lane is left at a task boundary its remaining segments
+// become solo tasks of `chunk` segments.
 int build_long_index(const dtans_container_view *c, int seg_threshold, uint64_t max_words, int chunk,
-                     uint64_t stage_words, LongIndex &out);
+                     LongIndex &out);
 
 }  // namespace dtans

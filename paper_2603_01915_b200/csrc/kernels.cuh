@@ -61,7 +61,6 @@ constexpr int kSlots = 4096;
 constexpr int kMaxWarps = 32;  // warps per CTA of the main kernel
 constexpr int kMaxRing = 2;     // staging buffers per warp (a double-buffered ring)
 constexpr int kMaxChunk = 16;   // slices per chunk
-constexpr uint32_t kTaskK = 0xFF;  // ChunkRec k of a staged long-slice task
 constexpr uint32_t kTabBytes = 2 * kSlots * 4;
 constexpr uint32_t kDeltaInlineEsc = 0xFFFF0000u;  // inline deltas: F = 0xFFFF marks an escape
 
@@ -544,12 +543,21 @@ __device__ __forceinline__ void fold(uint32_t d, uint32_t bm1, uint32_t D, uint3
 // One segment that is not the final one of the slice (some lane folds
 // digits).  kHot: every lane is active and not in its last segment (all
 // 4 pairs valid, all lanes load/extract), so the per-lane predicates vanish.
-template <typename V, bool kDecode, bool kHot, bool kDIn, class Src>
+// Products of a hot segment whose accumulation is deferred: its four
+// value symbols and gathered x, accumulated (in order) by the final segment
+// after that segment has issued its own gathers, so the last full segment's
+// x latency overlaps the final segment's decode.
+template <typename V> struct Pend4 {
+    typename ValueTraits<V>::Bits vs[4];
+    V xv[4];
+};
+
+template <typename V, bool kDecode, bool kHot, bool kDIn, class Src, bool kDefer = false>
 __device__ __forceinline__ void full_segment(const KernelArgs &a, const Ctx &C, const V *__restrict__ x,
                                              const Src &src, const uint32_t j, const uint32_t n,
                                              const uint32_t nseg, uint32_t &w0, uint32_t &w1, uint32_t &w2,
                                              uint32_t &d, uint32_t &r, uint32_t &cur, uint32_t &col, V &acc,
-                                             int64_t &out_pos, const int lane)
+                                             int64_t &out_pos, const int lane, Pend4<V> *pd = nullptr)
 {
     using T = ValueTraits<V>;
     using Bits = typename T::Bits;
@@ -610,7 +618,13 @@ __device__ __forceinline__ void full_segment(const KernelArgs &a, const Ctx &C, 
             r = ext1 ? r2h : r2l;
             w2 = lw2;
         }
-        if (!kDecode) {
+        if (kDefer) {
+#pragma unroll
+            for (int p = 0; p < 4; p++) {
+                pd->vs[p] = vs[p];
+                pd->xv[p] = xv[p];
+            }
+        } else if (!kDecode) {
 #pragma unroll
             for (int p = 0; p < 4; p++) {
                 if (kHot || 8u * j + 2u * p < n) acc = T::add(acc, T::mul(T::from_bits(vs[p]), xv[p]));
@@ -641,10 +655,10 @@ template <typename V> struct LaneState {
 // with any valid position in the warp (compile-time, so no per-pair
 // branches); slots past them are pads that only matter if they can escape,
 // in which case the caller passes NP = 4.
-template <typename V, bool kDecode, bool kDIn, int NP, class Src>
+template <typename V, bool kDecode, bool kDIn, int NP, class Src, bool kPend = false>
 __device__ __forceinline__ void final_segment(const KernelArgs &a, const Ctx &C, const V *__restrict__ x,
                                               const Src &src, const uint32_t jf, const uint32_t n,
-                                              LaneState<V> &st)
+                                              LaneState<V> &st, const Pend4<V> *pd = nullptr)
 {
     using T = ValueTraits<V>;
     using Bits = typename T::Bits;
@@ -665,6 +679,24 @@ __device__ __forceinline__ void final_segment(const KernelArgs &a, const Ctx &C,
     // the event over the NP pairs only (pads past them never escape)
     payload_event<T, Src, NP>(C, src, st.cur, act, e, ds, vs);
     const uint32_t base = 8u * jf;
+    if (kPend) {
+        // gathers first, then the previous segment's products, then ours
+        V xv[NP];
+#pragma unroll
+        for (int p = 0; p < NP; p++) {
+            xv[p] = V(0);
+            if (base + 2u * p < n) {
+                st.col += ds[p];
+                xv[p] = __ldg(x + min(st.col, C.cols_m1));
+            }
+        }
+#pragma unroll
+        for (int p = 0; p < 4; p++) st.acc = T::add(st.acc, T::mul(T::from_bits(pd->vs[p]), pd->xv[p]));
+#pragma unroll
+        for (int p = 0; p < NP; p++)
+            if (base + 2u * p < n) st.acc = T::add(st.acc, T::mul(T::from_bits(vs[p]), xv[p]));
+        return;
+    }
 #pragma unroll
     for (int p = 0; p < NP; p++) {
         if (base + 2u * p < n) {
@@ -686,7 +718,10 @@ __device__ __forceinline__ void final_segment(const KernelArgs &a, const Ctx &C,
 // so no digits are folded and no checks/unconditional loads happen, and
 // pairs past the longest row are skipped (pads need lookups only when they
 // may escape).  Returns false if the cursor ran past `end` (corrupt slice).
-template <typename V, bool kDecode, bool kDIn, class Src>
+// kPend (SpMV): when every lane is hot up to a one-pair final segment,
+// that segment's gather goes out before the last full segment's products are
+// accumulated (Pend4), so the two x latencies overlap.
+template <typename V, bool kDecode, bool kDIn, class Src, bool kPend = false>
 __device__ __forceinline__ bool decode_range(const KernelArgs &a, const Ctx &C, const V *__restrict__ x,
                                              Src &src, const uint32_t end, const uint32_t n,
                                              const uint32_t max_nseg, const uint32_t min_nseg, const uint32_t np,
@@ -698,6 +733,24 @@ __device__ __forceinline__ bool decode_range(const KernelArgs &a, const Ctx &C, 
     // where some lane does (per-lane predicates)
     uint32_t j = j0;
     const uint32_t jhot = min(jfull, min_nseg > 0 ? min_nseg - 1u : 0u);
+    if (kPend && !kDecode && j1 == max_nseg && jhot == jfull && jfull > j0 && np == 1u) {
+        // hot up to a short final segment: its gathers go out before the
+        // last full segment's products are accumulated
+        for (; j + 1 < jfull; j++) {
+            src.prepare(st.cur);
+            full_segment<V, kDecode, true, kDIn>(a, C, x, src, j, n, nseg, st.w0, st.w1, st.w2, st.d, st.r, st.cur,
+                                                 st.col, st.acc, st.out_pos, lane);
+            if (st.cur > end) return false;  // uniform
+        }
+        Pend4<V> pd;
+        src.prepare(st.cur);
+        full_segment<V, kDecode, true, kDIn, Src, !kDecode>(a, C, x, src, j, n, nseg, st.w0, st.w1, st.w2, st.d,
+                                                             st.r, st.cur, st.col, st.acc, st.out_pos, lane, &pd);
+        if (st.cur > end) return false;
+        src.prepare(st.cur);
+        final_segment<V, kDecode, kDIn, 1, Src, !kDecode>(a, C, x, src, max_nseg - 1, n, st, &pd);
+        return true;
+    }
     for (; j < jhot; j++) {
         src.prepare(st.cur);
         full_segment<V, kDecode, true, kDIn>(a, C, x, src, j, n, nseg, st.w0, st.w1, st.w2, st.d, st.r, st.cur,
@@ -796,6 +849,22 @@ template <typename V> __device__ __forceinline__ void st_stream(V *p, V v)
 }
 
 // consumption check (container.py:499-500) and column bound, one vote
+// The same checks folded into a per-lane bit set (bit 0: consumption, bit 1:
+// column bound), voted once per chunk (flush_bad) instead of once per slice.
+__device__ __forceinline__ uint32_t bad_bits(const Ctx &C, bool ok, uint32_t cur, uint32_t end, uint32_t n,
+                                             uint32_t col)
+{
+    return (!ok || cur != end ? 1u : 0u) | (n > 0 && col > C.cols_m1 ? 2u : 0u);
+}
+__device__ __forceinline__ void flush_bad(const KernelArgs &a, uint32_t &bad, int lane)
+{
+    if (__any_sync(0xFFFFFFFFu, bad != 0u)) {  // rare
+        const uint32_t all = __reduce_or_sync(0xFFFFFFFFu, bad);
+        if (lane == 0) atomicOr(a.err, all);
+    }
+    bad = 0u;
+}
+
 __device__ __forceinline__ void report(const KernelArgs &a, const Ctx &C, bool ok, uint32_t cur, uint32_t end,
                                        uint32_t n, uint32_t col, int lane)
 {
@@ -809,11 +878,11 @@ __device__ __forceinline__ void report(const KernelArgs &a, const Ctx &C, bool o
 
 // One slice of a staged chunk: y (or decode positions) from global memory,
 // everything else from shared memory.
-template <typename V, bool kDecode, bool kHasY, bool kDIn, bool kScaled>
+template <typename V, bool kDecode, bool kHasY, bool kDIn, bool kScaled, bool kPend>
 __device__ __forceinline__ void decode_slice(const KernelArgs &a, const Ctx &C, const V *__restrict__ x,
                                              SmemSrc src, const uint32_t end, const uint32_t meta,
                                              const uint32_t n, const uint32_t row, const int lane, const V scale,
-                                             double &wsum)
+                                             double &wsum, uint32_t &bad)
 {
     using T = ValueTraits<V>;
     const bool inrow = row < (uint32_t)a.rows;
@@ -826,11 +895,17 @@ __device__ __forceinline__ void decode_slice(const KernelArgs &a, const Ctx &C, 
     if (kHasY && inrow) yv = ld_stream(reinterpret_cast<const V *>(a.y) + orow);
     LaneState<V> st;
     st.out_pos = 0;
-    if (kDecode && inrow) st.out_pos = __ldg(a.row_start + row);
-    init_state<V>(C, src, n, st);
-    const bool ok =
-        decode_range<V, kDecode, kDIn>(a, C, x, src, end, n, max_nseg, min_nseg, np, 0u, max_nseg, st, lane);
-    report(a, C, ok, st.cur, end, n, st.col, lane);
+    st.cur = 0;
+    st.col = 0;
+    st.acc = V(0);
+    bool ok = true;
+    if (max_nseg != 0u) {  // uniform; an all-empty slice has no words (y' = +0.0 + y)
+        if (kDecode && inrow) st.out_pos = __ldg(a.row_start + row);
+        init_state<V>(C, src, n, st);
+        ok = decode_range<V, kDecode, kDIn, SmemSrc, kPend>(a, C, x, src, end, n, max_nseg, min_nseg, np, 0u,
+                                                            max_nseg, st, lane);
+    }
+    bad |= bad_bits(C, ok, st.cur, end, n, st.col);
     if (!kDecode && inrow) {
         V res = kHasY ? T::add(st.acc, yv) : st.acc;
         if (kScaled) {
@@ -871,68 +946,6 @@ __device__ __forceinline__ void cp_async16(uint32_t dst, const void *src)
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
-// A staged long-slice task (api.cu assemble_task): segments [j0, j1) of a
-// long slice from its staged blob
-//   [slice, j0, j1, part, nwin, max_nseg, min_nseg | np << 16 | last << 24, ckw]
-//   [32 row_symbols][resume record: mask, 0, 6 words per active lane][nwin words]
-// (checkpoints.cpp walk_staged).  Single-task slices write y' here; the
-// others leave a per-lane partial sum for dtans_finalize_kernel.
-template <typename V, bool kDecode, bool kHasY, bool kDIn, bool kScaled>
-__device__ __forceinline__ void decode_staged_task(const KernelArgs &a, const Ctx &C, const V *__restrict__ x,
-                                                   const uint32_t buf, const int lane, const V scale, double &wsum)
-{
-    using T = ValueTraits<V>;
-    const uint4 h0 = ld_shared_v4(buf);
-    const uint4 h1 = ld_shared_v4(buf + 16u);
-    const uint32_t slice = h0.x, j0 = h0.y, j1 = h0.z, part = h0.w;
-    const uint32_t nwin = h1.x, max_nseg = h1.y;
-    const uint32_t min_nseg = h1.z & 0xFFFFu, np = (h1.z >> 16) & 0xFFu;
-    const bool last = (h1.z >> 24) != 0u;
-    const uint32_t ckw = h1.w;
-    const uint32_t n = sh32(buf + 32u + (uint32_t)lane * 4u);
-    const uint32_t row = slice * kSliceRows + (uint32_t)lane;
-    const bool inrow = row < (uint32_t)a.rows;
-    SmemSrc src{buf + (40u + ckw) * 4u};
-    LaneState<V> st;
-    st.out_pos = 0;
-    if (ckw == 0u) {
-        init_state<V>(C, src, n, st);
-    } else {
-        const uint32_t mask = sh32(buf + 160u);
-        const bool active = (mask >> lane) & 1u;
-        const uint32_t pk = buf + 168u + 24u * (uint32_t)__popc(mask & C.lt);
-        const uint2 q0 = ld_shared_v2(pk), q1 = ld_shared_v2(pk + 8u), q2 = ld_shared_v2(pk + 16u);
-        st.w0 = active ? q0.x : 0u;
-        st.w1 = active ? q0.y : 0u;
-        st.w2 = active ? q1.x : 0u;
-        st.d = active ? q1.y : 0u;
-        st.r = active ? q2.x : 1u;
-        st.col = active ? q2.y : 0u;
-        st.cur = 0u;
-        st.acc = V(0);
-    }
-    // decoding: every segment before j0 of an active lane was full (4 pairs)
-    if (kDecode && inrow) st.out_pos = __ldg(a.row_start + row) + 4ll * j0;
-    const bool ok = decode_range<V, kDecode, kDIn>(a, C, x, src, nwin, n, max_nseg, min_nseg, np, j0, j1, st, lane);
-    report(a, C, ok, st.cur, nwin, last ? n : 0u, st.col, lane);
-    if (kDecode) return;
-    if (last && j0 == 0u) {
-        // the slice is this single task: y' = acc + y directly
-        if (inrow) {
-            const uint32_t orow = a.row_map != nullptr ? __ldg(a.row_map + row) : row;
-            V res = st.acc;
-            if (kHasY) res = T::add(res, ld_stream(reinterpret_cast<const V *>(a.y) + orow));
-            if (kScaled) {
-                res = T::mul(res, scale);
-                wsum = __dadd_rn(wsum, __dmul_rn((double)res, (double)res));
-            }
-            st_stream(reinterpret_cast<V *>(a.out) + orow, res);
-        }
-    } else {
-        reinterpret_cast<V *>(a.partials)[(size_t)part * 32 + lane] = st.acc;
-    }
-}
-
 // Chunk staging (lane 0): one cp.async.bulk of the chunk's blob completing
 // on the buffer's mbarrier.  The previous contents were consumed by this
 // warp's LDS before the __syncwarp that precedes the call (the same WAR
@@ -964,9 +977,10 @@ struct WarpCtl {
 // Persistent kernel, one CTA of 32 warps per SM: tables -> shared memory once,
 // then every warp walks chunks (static stride or atomic tickets) through its
 // TMA ring.
-// kTasks: the chunk list also holds staged long-slice tasks (a separate
-// instantiation, so matrices without long slices do not pay its registers).
-template <typename V, bool kDecode, bool kHasY, bool kDIn, bool kScaled = false, bool kTasks = false>
+// kPend: decode_range may defer the last hot segment's products past a
+// short final segment's gathers (a separate instantiation, chosen at upload
+// for matrices where most slices take that path: it costs registers).
+template <typename V, bool kDecode, bool kHasY, bool kDIn, bool kScaled = false, bool kPend = false>
 __global__ void __launch_bounds__(kMaxWarps * 32, 1) dtans_kernel(const KernelArgs a)
 {
     constexpr int kWarps = kMaxWarps;
@@ -1029,16 +1043,13 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) dtans_kernel(const KernelAr
         ctl->pend_c = claim();
     }
     __syncwarp();
+    uint32_t bad = 0u;  // this chunk's failed checks (bad_bits)
     for (uint32_t it = 0;; it++) {
         const uint32_t b = it & (kMaxRing - 1u);
         mbar_wait(bars + 8u * b, (it / kMaxRing) & 1u);
         const uint2 md = ld_shared_v2(metas + 8u * b);
         const uint32_t s0 = md.x, k = md.y;
         if (k == 0) break;  // uniform: this warp's chunks are exhausted
-        if (kTasks && k == kTaskK) {  // uniform: a staged long-slice task
-            decode_staged_task<V, kDecode, kHasY, kDIn, kScaled>(a, C, x, bufs + b * (uint32_t)a.bufb, lane, scale,
-                                                                  wsum);
-        } else {
         // the chunk's addresses live in the warp's control block and are
         // re-read per slice (one LDS.128) instead of occupying registers
         // across the decode
@@ -1056,11 +1067,12 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) dtans_kernel(const KernelAr
             const uint32_t dnext = meta & 0xFFFFu;
             const uint32_t n = sh32(cs.y + i * 128u + (uint32_t)lane * 4u);
             const SmemSrc src{cs.z + dcur * 4u};
-            decode_slice<V, kDecode, kHasY, kDIn, kScaled>(a, C, x, src, dnext - dcur, meta, n,
-                                                            (cs.w + i) * kSliceRows + (uint32_t)lane, lane, scale, wsum);
+            decode_slice<V, kDecode, kHasY, kDIn, kScaled, kPend>(a, C, x, src, dnext - dcur, meta, n,
+                                                            (cs.w + i) * kSliceRows + (uint32_t)lane, lane, scale, wsum,
+                                                            bad);
             dcur = dnext;
         }
-        }
+        flush_bad(a, bad, lane);
         __syncwarp();
         if (lane == 0) {
 #if DTANS_RECASYNC
@@ -1090,9 +1102,12 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) dtans_kernel(const KernelAr
 constexpr int kTaskWarps = DTANS_TASK_WARPS;  // task kernel CTA size (warps)
 
 // Long-slice tasks: each warp decodes segments [j0, j1) of one slice from a
-// checkpoint (or the init events), reading the stream from global memory,
-// and writes its 32 per-lane partial sums (or, when decoding, the columns
-// and value bits of those segments directly).
+// checkpoint (or the init events), reading the stream from global memory
+// (the task's words are prefetched into L1 first), and writes its 32
+// per-lane partial sums (or, when decoding, the columns and value bits of
+// those segments directly).  Staging the task words in shared memory instead
+// (whole tasks, or a streamed window of cp.async.bulk quarters) measured
+// slower: the shared-memory carve-out costs the x gathers their L1 (DESIGN 5c).
 template <typename V, bool kDecode, bool kDIn>
 __global__ void __launch_bounds__(kTaskWarps * 32, 1024 / (kTaskWarps * 32)) dtans_task_kernel(const KernelArgs a)
 {
@@ -1107,7 +1122,9 @@ __global__ void __launch_bounds__(kTaskWarps * 32, 1024 / (kTaskWarps * 32)) dta
     const uint32_t warps = blockDim.x >> 5;
     const Ctx C = make_ctx<V>(a, lane);
     const V *__restrict__ x = reinterpret_cast<const V *>(a.x);
+#if !DTANS_GMEM_CS
     const unsigned long long pol = policy_evict_first();
+#endif
     // power iteration (sumsq_out set): single-task slices are final here, so
     // they are scaled and their squares summed like the main kernel's rows
     const V scale = a.sumsq_in != nullptr ? (V)__ddiv_rn(1.0, __dsqrt_rn(*a.sumsq_in)) : V(1);
@@ -1119,19 +1136,22 @@ __global__ void __launch_bounds__(kTaskWarps * 32, 1024 / (kTaskWarps * 32)) dta
         const uint32_t n = inrow ? __ldg(a.row_symbols + row) : 0u;
         uint32_t max_nseg, min_nseg, np;
         slice_shape(C, n, max_nseg, min_nseg, np);
+        // the task's words [cur0, cur1) of the slice (a first task also reads
+        // the init words from 0); positions are task-relative
+        const uint32_t w0 = tk.ck == 0xFFFFFFFFu ? 0u : tk.cur0;
+        const uint64_t g0 = __ldg(a.directory + tk.slice) + w0;
+        const uint32_t ntw = tk.cur1 - w0;
 #if DTANS_GMEM_CS
-        GmemSrc src{a.stream + __ldg(a.directory + tk.slice)};
+        GmemSrc src{a.stream + g0};
 #else
-        GmemSrc src{a.stream + __ldg(a.directory + tk.slice), pol};
+        GmemSrc src{a.stream + g0, pol};
 #endif
         {
             // pull the task's stream words into L1 up front (coalesced line
             // prefetches) so the loads on the serial per-segment chain hit L1
-            const uint32_t w0 = tk.ck == 0xFFFFFFFFu ? 0u : tk.cur0;
-            const char *b = reinterpret_cast<const char *>(src.p + w0);
-            const char *e = reinterpret_cast<const char *>(src.p + tk.cur1);
-            for (const char *q = b + 128 * lane; q < e; q += 128 * 32)
-                asm volatile("prefetch.global.L1 [%0];" ::"l"(q));
+            const char *b = reinterpret_cast<const char *>(src.p);
+            const char *e = reinterpret_cast<const char *>(src.p + ntw);
+            for (const char *q = b + 128 * lane; q < e; q += 128 * 32) asm volatile("prefetch.global.L1 [%0];" ::"l"(q));
         }
         LaneState<V> st;
         st.out_pos = 0;
@@ -1147,14 +1167,14 @@ __global__ void __launch_bounds__(kTaskWarps * 32, 1024 / (kTaskWarps * 32)) dta
             st.d = active ? __ldg(p + 3) : 0u;
             st.r = active ? __ldg(p + 4) : 1u;
             st.col = active ? __ldg(p + 5) : 0u;
-            st.cur = tk.cur0;
+            st.cur = 0u;
             st.acc = V(0);
         }
         // decoding: every segment before j0 of an active lane was full (4 pairs)
         if (kDecode && inrow) st.out_pos = __ldg(a.row_start + row) + 4ll * tk.j0;
-        const bool ok = decode_range<V, kDecode, kDIn>(a, C, x, src, tk.cur1, n, max_nseg, min_nseg, np, tk.j0,
-                                                       tk.j1, st, lane);
-        report(a, C, ok, st.cur, tk.cur1, tk.last ? n : 0u, st.col, lane);
+        const bool ok = decode_range<V, kDecode, kDIn>(a, C, x, src, ntw, n, max_nseg, min_nseg, np, tk.j0, tk.j1,
+                                                       st, lane);
+        report(a, C, ok, st.cur, ntw, tk.last ? n : 0u, st.col, lane);
         if (!kDecode) {
             if (tk.last && tk.j0 == 0) {
                 // the slice is this single task: y' = acc + y directly
