@@ -37,7 +37,7 @@ if a.full:
     hdr, units, vals = raw[0], raw[1], raw[2]
     rd = dict(zip(hdr, vals)); ud = dict(zip(hdr, units))
     keys = ["Kernel Name", "gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
-            "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "sm__inst_executed.sum",
+            "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "sm__inst_executed.sum", "smsp__inst_executed.sum",
             "smsp__issue_active.avg.pct_of_peak_sustained_active", "sm__warps_active.avg.pct_of_peak_sustained_active",
             "launch__registers_per_thread", "launch__block_size", "launch__grid_size",
             "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum",
