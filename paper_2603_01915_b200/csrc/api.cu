@@ -456,10 +456,21 @@ void parallel_for(size_t n, F &&f)
 
 // One chunk blob (kernels.cuh ChunkRec): slice metadata words, the slices'
 // row_symbols, their stream words -- copied from the container arrays.
-void assemble_chunk(const dtans_container_view *c, const dev::ChunkRec &r, bool pads_ok, uint32_t *p)
+void assemble_chunk(const dtans_container_view *c, const dev::ChunkRec &r, const dev::ChunkRec *next, bool pads_ok,
+                    uint32_t *p)
 {
     const int64_t s0 = r.s0, k = r.kw & 0xFF;
     const uint64_t base = c->directory[s0];
+    // the embedded record of the chunk the same warp buffer takes next
+    if (next) {
+        p[0] = (uint32_t)next->off;
+        p[1] = (uint32_t)(next->off >> 32);
+        p[2] = next->s0;
+        p[3] = next->kw;
+    } else {
+        p[0] = p[1] = p[2] = p[3] = 0u;
+    }
+    p += 4;
     for (int64_t i = 0; i < k; i++) {
         // slice metadata word (kernels.cuh slice_meta)
         const int64_t sr0 = (s0 + i) * kSlice;
@@ -473,7 +484,7 @@ void assemble_chunk(const dtans_container_view *c, const dev::ChunkRec &r, bool 
         const uint32_t np = pads_ok && mseg > 0 ? (maxn - 8u * (mseg - 1u)) / 2u : 4u;
         p[i] = dev::slice_meta((uint32_t)(c->directory[s0 + i + 1] - base), mseg, minseg, np);
     }
-    const uint32_t hw = dev::chunk_hdr_words((uint32_t)k);
+    const uint32_t hw = dev::chunk_hdr_words((uint32_t)k) - 4u;
     for (uint32_t i = (uint32_t)k; i < hw; i++) p[i] = 0u;
     p += hw;
     const int64_t r0 = s0 * kSlice, r1 = std::min<int64_t>((s0 + k) * kSlice, c->rows);
@@ -624,7 +635,8 @@ extern "C" int dtans_upload(const dtans_container_view *c, int device, dtans_dev
     }
     LongIndex li;
     {
-        const uint64_t max_words = (uint64_t)(sp.bufb - 16 - 128) / 4;
+        // a slice is long when even a one-slice chunk (chunk_words) overflows a buffer
+        const uint64_t max_words = (uint64_t)(sp.bufb - 4 * (int)dev::chunk_hdr_words(1) - 128) / 4;
         const int rc0 = build_long_index(c, long_seg, max_words, std::max(1, chunk), li);
         if (rc0) {
             delete h;
@@ -665,8 +677,10 @@ extern "C" int dtans_upload(const dtans_container_view *c, int device, dtans_dev
                                 : std::max<int64_t>(1, std::min<int64_t>(dev::kMaxChunk,
                                                                           nsl / ((int64_t)sms * dev::kMaxWarps * 4)));
         uint64_t blob_words = 0;
+        bool overflow = false;  // a chunk larger than a staging buffer (planner bug: fail loudly)
         auto push = [&](int64_t s0, int64_t k) {
             const uint64_t w = chunk_words(c->directory, s0, k);
+            if (4 * w > (uint64_t)sp.bufb) overflow = true;
             h->chunks.push_back(dev::ChunkRec{blob_words, (uint32_t)s0, (uint32_t)k | (uint32_t)w << 8});
             blob_words += w;
         };
@@ -694,6 +708,13 @@ extern "C" int dtans_upload(const dtans_container_view *c, int device, dtans_dev
             }
         }
         h->blob_words = blob_words;
+        if (overflow) {
+            delete h;
+            return fail(DTANS_E_PARAM, "internal: a chunk does not fit a staging buffer");
+        }
+        // static plans embed each chunk's successor in the same warp buffer
+        // (chunk + 2 x the full grid's stride) in its blob
+        h->base.embed_stride = dyn ? 0u : (uint32_t)(sms * dev::kMaxWarps);
         // the pending-products instantiation pays off where most staged
         // slices are hot up to a one-pair final segment (kernels.cuh
         // decode_range kPend, e.g. the 5-point Laplacian); elsewhere its
@@ -788,7 +809,9 @@ extern "C" int dtans_upload(const dtans_container_view *c, int device, dtans_dev
             parallel_for(qe - q, [&](size_t lo, size_t hi) {
                 for (size_t i = lo; i < hi; i++) {
                     const dev::ChunkRec &r = h->chunks[q + i];
-                    assemble_chunk(c, r, pads_ok, dst + (r.off - off0));
+                    const size_t nq = q + i + (size_t)dev::kMaxRing * h->base.embed_stride;
+                    assemble_chunk(c, r, h->base.embed_stride && nq < nch ? &h->chunks[nq] : nullptr, pads_ok,
+                                   dst + (r.off - off0));
                 }
             });
             if (!up.submit(h->d_blob + off0, words * 4)) rc = cuda_fail(up.err, "upload chunk blobs");

@@ -43,9 +43,6 @@
 #include "checkpoints.h"
 
 // Build-time switches for A/B experiments (DESIGN 5c); the defaults are the product.
-#ifndef DTANS_RECASYNC
-#define DTANS_RECASYNC 0  // 1: chunk records prefetched with cp.async a chunk ahead (banded -2.6%: off)
-#endif
 #ifndef DTANS_GMEM_CS
 #define DTANS_GMEM_CS 0  // 1: long-slice stream words via ld.global.cs.nc (R-MAT +2.5%: off)
 #endif
@@ -84,7 +81,10 @@ template <> struct ValueTraits<float> {
 
 // A chunk: slices [s0, s0 + k) (k = kw & 0xFF) stored as one contiguous
 // blob of kw >> 8 words at word offset `off` of the chunk-blob array:
-//   [hdr: k u32 slice words, padded to 4][row_symbols: k*32 u32][stream words, padded to 4]
+//   [next: the ChunkRec this warp stages into the same buffer after this
+//    chunk (chunk index + 2 x the static stride), zero when none or when the
+//    plan is dynamic][hdr: k u32 slice words, padded to 4]
+//   [row_symbols: k*32 u32][stream words, padded to 4]
 // hdr[i] describes slice s0+i (host-computed once at upload, slice_meta()):
 //   bits  0-15  directory[s0+i+1] - directory[s0]: the end of the slice's
 //               words relative to the chunk (container.py:296-317); the
@@ -99,7 +99,9 @@ struct __align__(16) ChunkRec {
     uint32_t s0;
     uint32_t kw;
 };
-__host__ __device__ constexpr uint32_t chunk_hdr_words(uint32_t k) { return (k + 3u) & ~3u; }
+// words before a chunk's row_symbols: the embedded next record (4 words),
+// then the k slice words padded to 4
+__host__ __device__ constexpr uint32_t chunk_hdr_words(uint32_t k) { return 4u + ((k + 3u) & ~3u); }
 constexpr uint32_t kMetaMaxNseg = 127u;  // max_nseg field width (7 bits)
 __host__ __device__ constexpr uint32_t slice_meta(uint32_t end_rel, uint32_t max_nseg, uint32_t min_nseg,
                                                   uint32_t np)
@@ -148,6 +150,7 @@ struct KernelArgs {
     const ChunkRec *chunks;
     uint32_t chunk_lo, chunk_hi;  // chunks of this launch
     int32_t dynamic;              // 1: atomic ticket counter instead of a static stride
+    uint32_t embed_stride;        // static stride (CTAs x warps) the blobs' next records were built for; 0: none
     uint32_t *work_counter;       // zeroed before every dynamic launch
 };
 
@@ -938,14 +941,6 @@ __device__ __forceinline__ uint2 ld_shared_v2(uint32_t addr)
     return v;
 }
 
-// 16-byte global -> shared copy that does not hold a register (LDGSTS):
-// lane 0 prefetches the next chunk record a whole chunk ahead of its use.
-__device__ __forceinline__ void cp_async16(uint32_t dst, const void *src)
-{
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\ncp.async.commit_group;" ::"r"(dst), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
-
 // Chunk staging (lane 0): one cp.async.bulk of the chunk's blob completing
 // on the buffer's mbarrier.  The previous contents were consumed by this
 // warp's LDS before the __syncwarp that precedes the call (the same WAR
@@ -972,6 +967,7 @@ struct WarpCtl {
     ChunkRec pend;
     uint32_t pend_c, next_static, pend_ok, pad;
     uint32_t hdr, rs, st, s0;  // the chunk being decoded (shared addresses), re-read per slice
+    uint32_t cidx[kMaxRing], pad2[4 - kMaxRing];  // embedded records: chunk index staged in each buffer
 };
 
 // Persistent kernel, one CTA of 32 warps per SM: tables -> shared memory once,
@@ -1012,12 +1008,15 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) dtans_kernel(const KernelAr
         if (a.sumsq_zero != nullptr && blockIdx.x == 0 && threadIdx.x == 0) *a.sumsq_zero = 0.0;
     }
 
-    // lane 0's claim pipeline: ticket -> chunk record (cp.async into the
-    // control block, a chunk ahead) -> staged buffer
+    // lane 0's claim pipeline.  Static plans built for this grid read the
+    // next chunk record from the blob just decoded (embedded, no global
+    // load); otherwise: ticket -> chunk record -> staged buffer.
+    const uint32_t G = gridDim.x * kWarps;
+    const bool emb = a.embed_stride == G && !a.dynamic;  // uniform
     auto claim = [&]() -> uint32_t {  // lane 0 only; >= chunk_hi: none
         if (a.dynamic) return a.chunk_lo + atomicAdd(a.work_counter, 1u);
         const uint32_t c = ctl->next_static;
-        ctl->next_static = c + gridDim.x * kWarps;
+        ctl->next_static = c + G;
         return c;
     };
     const uint32_t ctl_sh = sb + (uint32_t)a.off_ctl + (uint32_t)warp * (uint32_t)sizeof(WarpCtl);
@@ -1029,18 +1028,15 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) dtans_kernel(const KernelAr
             const bool v = c < a.chunk_hi;
             ChunkRec rc{};
             if (v) rc = a.chunks[c];
+            ctl->cidx[b] = c;
             stage_chunk(a, v, rc, bars + 8u * b, metas + 8u * b, bufs + b * (uint32_t)a.bufb);
         }
-        const uint32_t c = claim();
-        ctl->pend_ok = c < a.chunk_hi;
-        if (c < a.chunk_hi) {
-#if DTANS_RECASYNC
-            cp_async16(ctl_sh, a.chunks + c);
-#else
-            ctl->pend = a.chunks[c];
-#endif
+        if (!emb) {
+            const uint32_t c = claim();
+            ctl->pend_ok = c < a.chunk_hi;
+            if (c < a.chunk_hi) ctl->pend = a.chunks[c];
+            ctl->pend_c = claim();
         }
-        ctl->pend_c = claim();
     }
     __syncwarp();
     uint32_t bad = 0u;  // this chunk's failed checks (bad_bits)
@@ -1057,7 +1053,7 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) dtans_kernel(const KernelAr
         if (lane == 0) {
             const uint32_t buf = bufs + b * (uint32_t)a.bufb;
             const uint32_t hw = chunk_hdr_words(k);
-            st_shared_v4(ctl_cs, buf, buf + hw * 4u, buf + (hw + k * 32u) * 4u, s0);
+            st_shared_v4(ctl_cs, buf + 16u, buf + hw * 4u, buf + (hw + k * 32u) * 4u, s0);
         }
         __syncwarp();
         uint32_t dcur = 0;
@@ -1075,20 +1071,28 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) dtans_kernel(const KernelAr
         flush_bad(a, bad, lane);
         __syncwarp();
         if (lane == 0) {
-#if DTANS_RECASYNC
-            cp_async_wait_all();  // the pending record (issued a chunk ago)
-#endif
-            stage_chunk(a, ctl->pend_ok != 0u, ctl->pend, bars + 8u * b, metas + 8u * b, bufs + b * (uint32_t)a.bufb);
-            const uint32_t c = ctl->pend_c;
-            ctl->pend_ok = c < a.chunk_hi;
-            if (c < a.chunk_hi) {
-#if DTANS_RECASYNC
-                cp_async16(ctl_sh, a.chunks + c);
-#else
-                ctl->pend = a.chunks[c];
-#endif
+            const uint32_t buf = bufs + b * (uint32_t)a.bufb;
+            if (emb) {
+                // the record of the chunk this buffer takes next, embedded in
+                // the blob just decoded (read before the copy overwrites it)
+                const uint32_t c = ctl->cidx[b] + kMaxRing * G;
+                const bool v = c < a.chunk_hi;
+                ChunkRec rc{};
+                if (v) {
+                    const uint4 r = ld_shared_v4(buf);
+                    rc.off = (unsigned long long)r.x | (unsigned long long)r.y << 32;
+                    rc.s0 = r.z;
+                    rc.kw = r.w;
+                }
+                ctl->cidx[b] = c;
+                stage_chunk(a, v, rc, bars + 8u * b, metas + 8u * b, buf);
+            } else {
+                stage_chunk(a, ctl->pend_ok != 0u, ctl->pend, bars + 8u * b, metas + 8u * b, buf);
+                const uint32_t c = ctl->pend_c;
+                ctl->pend_ok = c < a.chunk_hi;
+                if (c < a.chunk_hi) ctl->pend = a.chunks[c];
+                ctl->pend_c = claim();
             }
-            ctl->pend_c = claim();
         }
         __syncwarp();
     }

@@ -45,11 +45,12 @@ def _fresh(c):
 
 def _pair_fits(c, bufb):
     """Whether two adjacent slices fit one staging buffer (api.cu
-    chunk_words: padded header + 2*32 row_symbols + the padded stream words)."""
+    chunk_words: next record + padded header + 2*32 row_symbols + the padded
+    stream words)."""
     d = np.asarray(c.directory, dtype=np.int64)
     if len(d) < 3:
         return False
-    words = 4 + 64 + ((d[2:] - d[:-2] + 3) & ~3)
+    words = 8 + 64 + ((d[2:] - d[:-2] + 3) & ~3)
     return bool((4 * words <= bufb).any())
 
 
