@@ -43,6 +43,9 @@
 #include "checkpoints.h"
 
 // Build-time switches for A/B experiments (DESIGN 5c); the defaults are the product.
+#ifndef DTANS_LATE_VS
+#define DTANS_LATE_VS 0  // 1: f64 value-dictionary loads after the escape probe (Laplacian +7%: off)
+#endif
 #ifndef DTANS_GMEM_CS
 #define DTANS_GMEM_CS 0  // 1: long-slice stream words via ld.global.cs.nc (R-MAT +2.5%: off)
 #endif
@@ -570,9 +573,22 @@ __device__ __forceinline__ void full_segment(const KernelArgs &a, const Ctx &C, 
     uint32_t so[8], e[8], ds[4];
     Bits vs[4];
     slot_offsets(C.tab, w0, w1, w2, so);
+    // f64 (DTANS_LATE_VS): the value symbols are read from the dictionary
+    // after the escape probe on the paths where no value escapes (the fast
+    // path carries only deltas), so the probe's two paths do not have to
+    // keep four 64-bit values in matching registers
+    constexpr bool kLate = DTANS_LATE_VS && T::kPayloadWords == 2;
 #pragma unroll
-    for (int p = 0; p < 4; p++)
-        lookup_pair<Bits, kDIn>(C, so[2 * p], so[2 * p + 1], e[2 * p], e[2 * p + 1], ds[p], vs[p]);
+    for (int p = 0; p < 4; p++) {
+        e[2 * p] = tab32(so[2 * p]);
+        e[2 * p + 1] = vtab32(so[2 * p + 1]);
+        ds[p] = kDIn ? (e[2 * p] >> 16) : tab32(C.dbase + (e[2 * p] >> 16));
+        if (!kLate) vs[p] = dict_bits<Bits>(C.vbase + (e[2 * p + 1] >> 16));
+    }
+    auto load_vs = [&]() __attribute__((always_inline)) {
+#pragma unroll
+        for (int p = 0; p < 4; p++) vs[p] = dict_bits<Bits>(C.vbase + (e[2 * p + 1] >> 16));
+    };
     // the rest of the segment once the symbols are final
     auto rest = [&](const uint32_t (&ds)[4], const Bits (&vs)[4]) __attribute__((always_inline)) {
         V xv[4];
@@ -637,11 +653,13 @@ __device__ __forceinline__ void full_segment(const KernelArgs &a, const Ctx &C, 
     bool dany;
     const int pk = payload_probe<T>(C, act, e, dany);
     if (pk == 2) {
+        if (kLate) load_vs();
         payload_slow<T>(C, src, cur, act, e, ds, vs);
         rest(ds, vs);
         return;
     }
     if (pk == 1) payload_fast<T>(C, src, cur, act, dany, e, ds, vs);
+    if (kLate) load_vs();
     rest(ds, vs);
 }
 
