@@ -47,7 +47,7 @@
 #define DTANS_LATE_VS 0  // 1: f64 value-dictionary loads after the escape probe (Laplacian +7%: off)
 #endif
 #ifndef DTANS_GMEM_CS
-#define DTANS_GMEM_CS 0  // 1: long-slice stream words via ld.global.cs.nc (R-MAT +2.5%: off)
+#define DTANS_GMEM_CS 0  // long-slice word loads: 0 L2 evict-first policy, 1 .cs (R-MAT +2.5%), 2 L1::evict_last, 3 __ldg
 #endif
 
 namespace dtans {
@@ -282,16 +282,25 @@ struct SmemSrc {
     __device__ __forceinline__ void prepare(uint32_t) {}
 };
 struct GmemSrc {
-    const uint32_t *p;  // &stream[directory[s]]
-#if DTANS_GMEM_CS
-    // streamed words: ld.global.cs.nc (evict-first in L1 and L2, so the
-    // gathered x stays cached), no cache-policy register
+    const uint32_t *p;  // the task's first word
+#if DTANS_GMEM_CS == 1
+    // ld.global.cs.nc: evict-first in L1 and L2, no cache-policy register
     __device__ __forceinline__ uint32_t operator()(uint32_t rel) const
     {
         uint32_t v;
         asm("ld.global.cs.nc.u32 %0, [%1];" : "=r"(v) : "l"(p + rel));
         return v;
     }
+#elif DTANS_GMEM_CS == 2
+    // ld.global.nc.L1::evict_last: the prefetched words stay in L1
+    __device__ __forceinline__ uint32_t operator()(uint32_t rel) const
+    {
+        uint32_t v;
+        asm("ld.global.nc.L1::evict_last.u32 %0, [%1];" : "=r"(v) : "l"(p + rel));
+        return v;
+    }
+#elif DTANS_GMEM_CS == 3
+    __device__ __forceinline__ uint32_t operator()(uint32_t rel) const { return __ldg(p + rel); }
 #else
     unsigned long long pol;  // L2 evict-first policy (streamed words)
     __device__ __forceinline__ uint32_t operator()(uint32_t rel) const
@@ -1144,7 +1153,7 @@ __global__ void __launch_bounds__(kTaskWarps * 32, 1024 / (kTaskWarps * 32)) dta
     const uint32_t warps = blockDim.x >> 5;
     const Ctx C = make_ctx<V>(a, lane);
     const V *__restrict__ x = reinterpret_cast<const V *>(a.x);
-#if !DTANS_GMEM_CS
+#if DTANS_GMEM_CS == 0
     const unsigned long long pol = policy_evict_first();
 #endif
     // power iteration (sumsq_out set): single-task slices are final here, so
@@ -1163,10 +1172,10 @@ __global__ void __launch_bounds__(kTaskWarps * 32, 1024 / (kTaskWarps * 32)) dta
         const uint32_t w0 = tk.ck == 0xFFFFFFFFu ? 0u : tk.cur0;
         const uint64_t g0 = __ldg(a.directory + tk.slice) + w0;
         const uint32_t ntw = tk.cur1 - w0;
-#if DTANS_GMEM_CS
-        GmemSrc src{a.stream + g0};
-#else
+#if DTANS_GMEM_CS == 0
         GmemSrc src{a.stream + g0, pol};
+#else
+        GmemSrc src{a.stream + g0};
 #endif
         {
             // pull the task's stream words into L1 up front (coalesced line

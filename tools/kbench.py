@@ -34,7 +34,11 @@ def main():
     ap.add_argument("--launches", type=int, default=0)
     ap.add_argument("--noy", action="store_true", help="y-less product (power-iteration form)")
     ap.add_argument("--cache", default=None, help="directory of encoded containers (CDTA + row map) to reuse")
+    ap.add_argument("--env", action="append", default=[], help="KEY=VALUE set before the upload (plan knobs)")
     a = ap.parse_args()
+    for kv in a.env:
+        k, v = kv.split("=", 1)
+        os.environ[k] = v
     spec = bench.Spec(a.config, a.scale)
     t0 = time.time()
     perm = None
