@@ -637,7 +637,27 @@ extern "C" int dtans_upload(const dtans_container_view *c, int device, dtans_dev
     {
         // a slice is long when even a one-slice chunk (chunk_words) overflows a buffer
         const uint64_t max_words = (uint64_t)(sp.bufb - 4 * (int)dev::chunk_hdr_words(1) - 128) / 4;
-        const int rc0 = build_long_index(c, long_seg, max_words, std::max(1, chunk), li);
+        // When rows are sorted by length (the skew toolkit's P*A) and most
+        // nonzeros already sit in long slices, every non-empty slice goes to
+        // the task kernel: one launch mixes the short, latency-bound slices
+        // with the long, issue-bound tasks (R-MAT sorted: -4.5 %).  An
+        // explicit DTANS_LONG_SEG wins.
+        int seg_thr = long_seg;
+        if (!e1) {
+            uint64_t nnz_long = 0, nnz_all = 0;
+            bool desc = true;
+            for (int64_t s = 0; s < nsl; s++) {
+                uint64_t z = 0;
+                for (int64_t i = s * kSlice; i < std::min<int64_t>((s + 1) * kSlice, c->rows); i++)
+                    z += c->row_symbols[i] / 2;
+                nnz_all += z;
+                const uint64_t words = ((c->directory[s + 1] + 3) & ~3ull) - (c->directory[s] & ~3ull);
+                if (cost[s] > (uint32_t)long_seg || words > max_words) nnz_long += z;
+                if (s > 0 && cost[s] > cost[s - 1]) desc = false;
+            }
+            if (desc && nnz_long * 2 >= nnz_all && nnz_all > 0) seg_thr = 0;
+        }
+        const int rc0 = build_long_index(c, seg_thr, max_words, std::max(1, chunk), li);
         if (rc0) {
             delete h;
             return rc0;

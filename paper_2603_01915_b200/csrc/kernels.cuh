@@ -285,31 +285,32 @@ struct GmemSrc {
     const uint32_t *p;  // the task's first word
 #if DTANS_GMEM_CS == 1
     // ld.global.cs.nc: evict-first in L1 and L2, no cache-policy register
-    __device__ __forceinline__ uint32_t operator()(uint32_t rel) const
+    __device__ __forceinline__ uint32_t at(const uint32_t *q) const
     {
         uint32_t v;
-        asm("ld.global.cs.nc.u32 %0, [%1];" : "=r"(v) : "l"(p + rel));
+        asm("ld.global.cs.nc.u32 %0, [%1];" : "=r"(v) : "l"(q));
         return v;
     }
 #elif DTANS_GMEM_CS == 2
     // ld.global.nc.L1::evict_last: the prefetched words stay in L1
-    __device__ __forceinline__ uint32_t operator()(uint32_t rel) const
+    __device__ __forceinline__ uint32_t at(const uint32_t *q) const
     {
         uint32_t v;
-        asm("ld.global.nc.L1::evict_last.u32 %0, [%1];" : "=r"(v) : "l"(p + rel));
+        asm("ld.global.nc.L1::evict_last.u32 %0, [%1];" : "=r"(v) : "l"(q));
         return v;
     }
 #elif DTANS_GMEM_CS == 3
-    __device__ __forceinline__ uint32_t operator()(uint32_t rel) const { return __ldg(p + rel); }
+    __device__ __forceinline__ uint32_t at(const uint32_t *q) const { return __ldg(q); }
 #else
     unsigned long long pol;  // L2 evict-first policy (streamed words)
-    __device__ __forceinline__ uint32_t operator()(uint32_t rel) const
+    __device__ __forceinline__ uint32_t at(const uint32_t *q) const
     {
         uint32_t v;
-        asm("ld.global.nc.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(p + rel), "l"(pol));
+        asm("ld.global.nc.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(q), "l"(pol));
         return v;
     }
 #endif
+    __device__ __forceinline__ uint32_t operator()(uint32_t rel) const { return at(p + rel); }
     __device__ __forceinline__ void prepare(uint32_t) {}
 };
 
@@ -483,21 +484,23 @@ __device__ __forceinline__ void payload_slow(const Ctx &C, const Src &src, uint3
                           (__popc(b3 & C.lt) << 3);
     const uint32_t total = __popc(b0) + (__popc(b1) << 1) + (__popc(b2) << 2) + (__popc(b3) << 3);
     if (pc) {
-        uint32_t off = cur + excl;
+        {
+            uint32_t off = cur + excl;
 #pragma unroll
-        for (int p = 0; p < NP; p++) {
-            if (e[2 * p] >= C.desc_min) {
-                ds[p] = src(off);
-                off += 1;
-            }
-            if (e[2 * p + 1] >= C.vesc_min) {
-                if (T::kPayloadWords == 2) {
-                    const uint32_t lo = src(off), hi = src(off + 1);
-                    vs[p] = (Bits)(((unsigned long long)hi << 32) | lo);
-                } else {
-                    vs[p] = (Bits)src(off);
+            for (int p = 0; p < NP; p++) {
+                if (e[2 * p] >= C.desc_min) {
+                    ds[p] = src(off);
+                    off += 1;
                 }
-                off += T::kPayloadWords;
+                if (e[2 * p + 1] >= C.vesc_min) {
+                    if (T::kPayloadWords == 2) {
+                        const uint32_t lo = src(off), hi = src(off + 1);
+                        vs[p] = (Bits)(((unsigned long long)hi << 32) | lo);
+                    } else {
+                        vs[p] = (Bits)src(off);
+                    }
+                    off += T::kPayloadWords;
+                }
             }
         }
     }
