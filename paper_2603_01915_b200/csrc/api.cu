@@ -36,6 +36,7 @@ struct dtans_dev {
     size_t io_bytes = 0;
     dev::KernelArgs base{};     // launch-invariant kernel arguments
     int ctas = 0, threads = 1024, smem = 0;
+    int warps = dev::kMaxWarps;  // warps per CTA of the main kernel
     int64_t launches = 0;
     int64_t staged_slices = 0;  // slices whose stream fits a ring buffer
     bool pend = false;          // main kernel instantiation with pending products (kernels.cuh kPend)
@@ -209,7 +210,7 @@ struct SmemPlan {
     std::vector<uint32_t> image;
 };
 
-SmemPlan plan_smem(const TableBlock &tb, int max_optin, int nring)
+SmemPlan plan_smem(const TableBlock &tb, int max_optin, int nring, int warps)
 {
     SmemPlan p;
     p.off_bars = 0;
@@ -245,8 +246,8 @@ SmemPlan plan_smem(const TableBlock &tb, int max_optin, int nring)
     p.off_bufs = (int32_t)off;
     const int64_t avail = (int64_t)max_optin - (int64_t)off - dev::kOverrunWords * 4;
     p.nring = nring;
-    p.bufb = (int32_t)std::max<int64_t>(0, avail / (dev::kMaxWarps * nring) / 16 * 16);
-    p.total = (int32_t)(off + (size_t)dev::kMaxWarps * nring * p.bufb + dev::kOverrunWords * 4);
+    p.bufb = (int32_t)std::max<int64_t>(0, avail / (warps * nring) / 16 * 16);
+    p.total = (int32_t)(off + (size_t)warps * nring * p.bufb + dev::kOverrunWords * 4);
     return p;
 }
 
@@ -341,9 +342,9 @@ int configure(dtans_dev *h, const TableBlock &tb, const SmemPlan &sp)
         h->solo_ctas = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)sms * std::max(pers, 1),
                                                                     ((int64_t)a.nsolo + 255) / 256));
     }
-    h->threads = dev::kMaxWarps * 32;
+    h->threads = h->warps * 32;
     h->smem = sp.total;
-    h->ctas = (int)std::max<int64_t>(1, std::min<int64_t>(sms, ((int64_t)h->chunks.size() + dev::kMaxWarps - 1) / dev::kMaxWarps));
+    h->ctas = (int)std::max<int64_t>(1, std::min<int64_t>(sms, ((int64_t)h->chunks.size() + h->warps - 1) / h->warps));
     int per_sm = 0;
     int rc = with_kernel<V>(tb.dinline, h->pend, [&](auto kspmv, auto kspmv0, auto kdec, auto kscaled) -> int {
         CK(cudaFuncSetAttribute(kscaled, cudaFuncAttributeMaxDynamicSharedMemorySize, h->smem), "cudaFuncSetAttribute");
@@ -380,7 +381,7 @@ int launch(dtans_dev *h, const V *x, const V *y, V *out, const int64_t *row_star
         a.chunk_hi = (uint32_t)c_hi;
     }
     const int64_t nch = (int64_t)a.chunk_hi - (int64_t)a.chunk_lo;
-    const int ctas = (int)std::max<int64_t>(1, std::min<int64_t>(h->sms, (nch + dev::kMaxWarps - 1) / dev::kMaxWarps));
+    const int ctas = (int)std::max<int64_t>(1, std::min<int64_t>(h->sms, (nch + h->warps - 1) / h->warps));
     if (a.dynamic) CK(cudaMemsetAsync(a.work_counter, 0, sizeof(uint32_t), st), "reset work counter");
     if (h->d_col_map && !decode_only) {
         if (c_lo <= 0) {  // once per product (the pipelined host path gathers before its first chunk)
@@ -400,7 +401,8 @@ int launch(dtans_dev *h, const V *x, const V *y, V *out, const int64_t *row_star
     a.sumsq_out = sumsq_out;
     a.sumsq_zero = sumsq_zero;
     if (nch > 0) {
-        with_kernel<V>(h->dinline, h->pend, [&](auto kspmv, auto kspmv0, auto kdec, auto kscaled) -> int {
+        // the pending-products instantiation has no row-map lookup
+        with_kernel<V>(h->dinline, h->pend && !h->d_row_map, [&](auto kspmv, auto kspmv0, auto kdec, auto kscaled) -> int {
             if (scaled)
                 kscaled<<<ctas, h->threads, h->smem, st>>>(a);
             else if (decode_only)
@@ -628,7 +630,19 @@ extern "C" int dtans_upload(const dtans_container_view *c, int device, dtans_dev
     // SM's 256 KB L1/shared array becomes L1 cache for the x gathers)
     const char *ek = getenv("DTANS_SMEM_KB");
     const int smem_cap = ek ? std::min(max_optin, atoi(ek) * 1024) : max_optin;
-    SmemPlan sp = plan_smem(tb, smem_cap, dev::kMaxRing);
+    // warps per CTA of the main kernel: 32, or fewer when the matrix has
+    // fewer slices than a full grid has warps -- their staging buffers are
+    // then larger, so small matrices' slices fit a buffer instead of going
+    // to the long-slice kernels (DTANS_WARPS forces it)
+    {
+        const char *ew = getenv("DTANS_WARPS");
+        int w = dev::kMaxWarps;
+        if (ew) w = std::max(1, std::min(dev::kMaxWarps, atoi(ew)));
+        else if (nsl < (int64_t)sms * dev::kMaxWarps)
+            w = (int)std::max<int64_t>(4, std::min<int64_t>(dev::kMaxWarps, (nsl + sms - 1) / sms));
+        h->warps = w;
+    }
+    SmemPlan sp = plan_smem(tb, smem_cap, dev::kMaxRing, h->warps);
     if (sp.bufb < 512) {
         delete h;
         return fail(DTANS_E_CUDA, "coding tables leave no shared memory for staging");
@@ -695,7 +709,7 @@ extern "C" int dtans_upload(const dtans_container_view *c, int device, dtans_dev
         const char *ek = getenv("DTANS_KCHUNK");
         const int64_t kcap = ek ? std::max(1, std::min(atoi(ek), dev::kMaxChunk))
                                 : std::max<int64_t>(1, std::min<int64_t>(dev::kMaxChunk,
-                                                                          nsl / ((int64_t)sms * dev::kMaxWarps * 4)));
+                                                                          nsl / ((int64_t)sms * h->warps * 4)));
         uint64_t blob_words = 0;
         bool overflow = false;  // a chunk larger than a staging buffer (planner bug: fail loudly)
         auto push = [&](int64_t s0, int64_t k) {
@@ -734,7 +748,7 @@ extern "C" int dtans_upload(const dtans_container_view *c, int device, dtans_dev
         }
         // static plans embed each chunk's successor in the same warp buffer
         // (chunk + 2 x the full grid's stride) in its blob
-        h->base.embed_stride = dyn ? 0u : (uint32_t)(sms * dev::kMaxWarps);
+        h->base.embed_stride = dyn ? 0u : (uint32_t)(sms * h->warps);
         // the pending-products instantiation pays off where most staged
         // slices are hot up to a one-pair final segment (kernels.cuh
         // decode_range kPend, e.g. the 5-point Laplacian); elsewhere its

@@ -923,7 +923,8 @@ __device__ __forceinline__ void decode_slice(const KernelArgs &a, const Ctx &C, 
     const uint32_t min_nseg = (meta >> 23) & 0x7Fu;
     const uint32_t np = (meta >> 30) + 1u;
     uint32_t orow = row;
-    if (a.row_map != nullptr && inrow) orow = __ldg(a.row_map + row);
+    // the pending-products instantiation never runs with a row map (api.cu)
+    if (!kPend && a.row_map != nullptr && inrow) orow = __ldg(a.row_map + row);
     V yv = V(0);
     if (kHasY && inrow) yv = ld_stream(reinterpret_cast<const V *>(a.y) + orow);
     LaneState<V> st;
@@ -1005,11 +1006,12 @@ struct WarpCtl {
 // TMA ring.
 // kPend: decode_range may defer the last hot segment's products past a
 // short final segment's gathers (a separate instantiation, chosen at upload
-// for matrices where most slices take that path: it costs registers).
+// for matrices where most slices take that path: it costs registers).  It is
+// never launched with a row map, so it drops the row-map lookup.
 template <typename V, bool kDecode, bool kHasY, bool kDIn, bool kScaled = false, bool kPend = false>
 __global__ void __launch_bounds__(kMaxWarps * 32, 1) dtans_kernel(const KernelArgs a)
 {
-    constexpr int kWarps = kMaxWarps;
+    const uint32_t kWarps = blockDim.x >> 5;  // kMaxWarps, fewer for small matrices (api.cu)
     const bool aligned = load_tables(a);
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
