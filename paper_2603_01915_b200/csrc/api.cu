@@ -342,7 +342,8 @@ int configure(dtans_dev *h, const TableBlock &tb, const SmemPlan &sp)
         h->solo_ctas = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)sms * std::max(pers, 1),
                                                                     ((int64_t)a.nsolo + 255) / 256));
     }
-    h->threads = h->warps * 32;
+    h->threads = dev::kMaxWarps * 32;  // all warps copy the tables; h->warps of them decode
+    a.work_warps = h->warps;
     h->smem = sp.total;
     h->ctas = (int)std::max<int64_t>(1, std::min<int64_t>(sms, ((int64_t)h->chunks.size() + h->warps - 1) / h->warps));
     int per_sm = 0;
@@ -934,7 +935,7 @@ extern "C" int dtans_info(const dtans_dev *h, int64_t *device_bytes, int32_t *ct
     if (!h) return fail(DTANS_E_PARAM, "null handle");
     if (device_bytes) *device_bytes = (int64_t)(h->d_bytes + h->long_bytes);
     if (ctas) *ctas = h->ctas;
-    if (warps_per_cta) *warps_per_cta = h->threads / 32;
+    if (warps_per_cta) *warps_per_cta = h->warps;
     if (smem_bytes) *smem_bytes = h->smem;
     return DTANS_OK;
 }

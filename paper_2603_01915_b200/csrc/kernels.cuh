@@ -154,6 +154,7 @@ struct KernelArgs {
     uint32_t chunk_lo, chunk_hi;  // chunks of this launch
     int32_t dynamic;              // 1: atomic ticket counter instead of a static stride
     uint32_t embed_stride;        // static stride (CTAs x warps) the blobs' next records were built for; 0: none
+    int32_t work_warps;           // main kernel: warps per CTA that decode (the CTA always has kMaxWarps)
     uint32_t *work_counter;       // zeroed before every dynamic launch
 };
 
@@ -1011,7 +1012,9 @@ struct WarpCtl {
 template <typename V, bool kDecode, bool kHasY, bool kDIn, bool kScaled = false, bool kPend = false>
 __global__ void __launch_bounds__(kMaxWarps * 32, 1) dtans_kernel(const KernelArgs a)
 {
-    const uint32_t kWarps = blockDim.x >> 5;  // kMaxWarps, fewer for small matrices (api.cu)
+    // warps that decode: kMaxWarps, fewer for small matrices (api.cu); the
+    // whole CTA still copies the tables in
+    const uint32_t kWarps = (uint32_t)a.work_warps;
     const bool aligned = load_tables(a);
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
@@ -1028,6 +1031,8 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) dtans_kernel(const KernelAr
         if (threadIdx.x == 0) atomicOr(a.err, 4u);
         return;
     }
+    if (kScaled && a.sumsq_zero != nullptr && blockIdx.x == 0 && threadIdx.x == 0) *a.sumsq_zero = 0.0;
+    if ((uint32_t)warp >= kWarps) return;  // helped with the table copy only
     const Ctx C = make_ctx<V>(a, lane);
     const V *__restrict__ x = reinterpret_cast<const V *>(a.x);
     V scale = V(1);
@@ -1037,7 +1042,6 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) dtans_kernel(const KernelAr
             const double q = *a.sumsq_in;
             scale = (V)__ddiv_rn(1.0, __dsqrt_rn(q));
         }
-        if (a.sumsq_zero != nullptr && blockIdx.x == 0 && threadIdx.x == 0) *a.sumsq_zero = 0.0;
     }
 
     // lane 0's claim pipeline.  Static plans built for this grid read the
