@@ -40,6 +40,7 @@ struct dtans_dev {
     int64_t launches = 0;
     int64_t staged_slices = 0;  // slices whose stream fits a ring buffer
     bool pend = false;          // main kernel instantiation with pending products (kernels.cuh kPend)
+    bool host_walk = false;     // long-slice index walked on the host (DTANS_GPU_WALK=0)
     std::vector<uint32_t> split_slices;  // slices whose rows sum several task partials
     size_t upload_staged_bytes = 0;  // bytes streamed through the pinned upload buffers
     int64_t upload_batches = 0;
@@ -285,8 +286,8 @@ int with_long_kernels(bool dinline, F &&f)
              dev::dtans_solo_kernel<V, false, false>, dev::dtans_solo_kernel<V, true, false>);
 }
 
-template <typename V>
-int configure(dtans_dev *h, const TableBlock &tb, const SmemPlan &sp)
+// The launch-invariant kernel arguments of the handle.
+void fill_args(dtans_dev *h, const TableBlock &tb, const SmemPlan &sp)
 {
     dev::KernelArgs &a = h->base;
     a.tables = h->d_tables;
@@ -320,6 +321,13 @@ int configure(dtans_dev *h, const TableBlock &tb, const SmemPlan &sp)
     a.chunk_lo = 0;
     a.chunk_hi = (uint32_t)h->chunks.size();
     h->dinline = tb.dinline;
+}
+
+template <typename V>
+int configure(dtans_dev *h, const TableBlock &tb, const SmemPlan &sp)
+{
+    dev::KernelArgs &a = h->base;
+    fill_args(h, tb, sp);
     int sms = 0;
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device), "sm count");
     h->sms = sms;
@@ -499,6 +507,56 @@ void assemble_chunk(const dtans_container_view *c, const dev::ChunkRec &r, const
     for (uint64_t i = nw; i < ((nw + 3) & ~3ull); i++) p[i] = 0u;
 }
 
+// The GPU pre-pass of the long-slice index (kernels.cuh dtans_walk_kernel):
+// one warp per long slice walks it once and writes the resume records into
+// the device pool (whose masks the host plan already holds) and the task
+// boundary cursors, which are copied back into the task lists here.
+template <typename V>
+int gpu_walk(dtans_dev *h, const TableBlock &tb, const SmemPlan &sp, const dtans_container_view *c, LongIndex &li,
+             uint32_t *d_pool, int chunk)
+{
+    fill_args(h, tb, sp);
+    const dev::KernelArgs &a = h->base;
+    const size_t nparts = li.nparts, nl = li.slices.size();
+    uint32_t *d_cur = nullptr;
+    CK(cudaMalloc(&d_cur, sizeof(uint32_t) * (nparts + nl)), "cudaMalloc(walk cursors)");
+    const int smem = (int)align_up((size_t)(a.off_img + a.table_bytes), 16);
+    const int blocks = (int)std::max<size_t>(1, std::min<size_t>((size_t)h->sms * 8, (nl + 7) / 8));
+    cudaError_t e = cudaSuccess;
+    auto run = [&](auto k) {
+        if ((e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)) != cudaSuccess) return;
+        k<<<blocks, 256, smem>>>(a, d_pool, d_cur, d_cur + nparts, (uint32_t)chunk);
+        e = cudaGetLastError();
+    };
+    if (tb.dinline) run(dev::dtans_walk_kernel<V, true>);
+    else run(dev::dtans_walk_kernel<V, false>);
+    std::vector<uint32_t> cur(nparts + nl);
+    if (e == cudaSuccess) e = cudaMemcpy(cur.data(), d_cur, sizeof(uint32_t) * cur.size(), cudaMemcpyDeviceToHost);
+    cudaFree(d_cur);
+    if (e != cudaSuccess) return cuda_fail(e, "checkpoint walk");
+    unsigned int err = 0;
+    CK(cudaMemcpy(&err, h->d_err, sizeof(err), cudaMemcpyDeviceToHost), "checkpoint walk status");
+    if (err & 4u) return fail(DTANS_E_CUDA, "checkpoint walk: shared-memory layout check failed");
+    // end cursor of every part: the next part's start in the same slice, or the slice's word count
+    std::vector<uint32_t> end(nparts, 0);
+    for (size_t i = 0; i < nl; i++) {
+        const LongSlice &ls = li.slices[i];
+        const uint32_t nw = (uint32_t)(c->directory[ls.slice + 1] - c->directory[ls.slice]);
+        if (cur[nparts + i] != nw) return fail(DTANS_E_CORRUPT, "long slice consumed an unexpected number of words");
+        for (uint32_t q = 0; q < ls.nparts; q++)
+            end[ls.part_base + q] = q + 1 < ls.nparts ? cur[ls.part_base + q + 1] : nw;
+    }
+    for (LongTask &t : li.tasks) {
+        t.cur0 = cur[t.part];
+        t.cur1 = end[t.part];
+    }
+    for (SoloTask &t : li.solo) {
+        t.cur0 = cur[t.part];
+        t.cur1 = end[t.part];
+    }
+    return DTANS_OK;
+}
+
 // Host->device copies through two pinned staging buffers on one stream:
 // the host fills buffer b while buffer b^1's cudaMemcpyAsync is in flight.
 struct PinnedUploader {
@@ -604,6 +662,7 @@ extern "C" int dtans_upload(const dtans_container_view *c, int device, dtans_dev
 
     dtans_dev *h = new dtans_dev();
     h->device = device;
+    h->sms = sms;
     h->rows = c->rows;
     h->cols = c->cols;
     h->nnz = c->nnz;
@@ -672,7 +731,11 @@ extern "C" int dtans_upload(const dtans_container_view *c, int device, dtans_dev
             }
             if (desc && nnz_long * 2 >= nnz_all && nnz_all > 0) seg_thr = 0;
         }
-        const int rc0 = build_long_index(c, seg_thr, max_words, std::max(1, chunk), li);
+        // the long-slice walk runs on the GPU (dtans_walk_kernel) unless
+        // DTANS_GPU_WALK=0 (the multithreaded host walk)
+        const char *eg = getenv("DTANS_GPU_WALK");
+        h->host_walk = eg && atoi(eg) == 0;
+        const int rc0 = build_long_index(c, seg_thr, max_words, std::max(1, chunk), h->host_walk, li);
         if (rc0) {
             delete h;
             return rc0;
@@ -883,12 +946,17 @@ extern "C" int dtans_upload(const dtans_container_view *c, int device, dtans_dev
             h->base.ck_pool = (const uint32_t *)(lb + tb_b);
             h->base.longs = (const LongSlice *)(lb + tb_b + pl_b);
             h->base.partials = lb + tb_b + pl_b + ls_b;
-            cp(lb, li.tasks.data(), li.tasks.size() * sizeof(LongTask));
-            cp((void *)h->base.solo, li.solo.data(), li.solo.size() * sizeof(SoloTask));
             // partial slots of solo tasks are written for one lane only
             zero(h->base.partials, pa_b);
             cp(lb + tb_b, li.pool.data(), li.pool.size() * 4);
             cp(lb + tb_b + pl_b, li.slices.data(), li.slices.size() * sizeof(LongSlice));
+            if (rc == DTANS_OK && !h->host_walk) {
+                h->base.nlong = (uint32_t)li.slices.size();
+                rc = c->precision == 8 ? gpu_walk<double>(h, tb, sp, c, li, (uint32_t *)(lb + tb_b), std::max(1, chunk))
+                                       : gpu_walk<float>(h, tb, sp, c, li, (uint32_t *)(lb + tb_b), std::max(1, chunk));
+            }
+            cp(lb, li.tasks.data(), li.tasks.size() * sizeof(LongTask));
+            cp((void *)h->base.solo, li.solo.data(), li.solo.size() * sizeof(SoloTask));
         }
     }
     if (rc == DTANS_OK)

@@ -217,6 +217,40 @@ void emit_solo(SliceWalk &W, int lane, uint32_t j, int chunk, SliceOut &o)
 
 // Global-memory tasks of `chunk` segments (and solo tasks once one lane is
 // left at a task boundary).
+// The same task structure without decoding (the GPU walk fills the cursors
+// and resume records, kernels.cuh dtans_walk_kernel): boundaries and masks
+// follow from the row lengths alone; records are zero placeholders of the
+// same sizes, masks included.
+void plan_fixed(const SliceWalk &W, int chunk, SliceOut &o)
+{
+    const uint32_t ntasks = (W.max_nseg + chunk - 1) / chunk;
+    for (uint32_t j = 0; j < W.max_nseg; j += chunk) {
+        const uint32_t amask = j ? W.active_mask(j) : 0u;
+        if (j && __builtin_popcount(amask) == 1) {
+            SoloTask t{};
+            t.lane = (uint32_t)__builtin_ctz(amask);
+            t.j0 = j;
+            t.j1 = std::min<uint32_t>(j + chunk, W.max_nseg);
+            t.part = o.nparts++;
+            t.ck = (uint32_t)o.pool.size();
+            o.pool.insert(o.pool.end(), 6, 0u);
+            o.solo.push_back(t);
+        } else {
+            LongTask t{};
+            t.j0 = j;
+            t.j1 = std::min<uint32_t>(j + chunk, W.max_nseg);
+            t.part = o.nparts++;
+            t.ck = j == 0 ? 0xFFFFFFFFu : (uint32_t)o.pool.size();
+            t.last = t.part + 1 == ntasks;
+            if (j) {
+                o.pool.push_back(amask);
+                o.pool.insert(o.pool.end(), 6 * (size_t)__builtin_popcount(amask), 0u);
+            }
+            o.tasks.push_back(t);
+        }
+    }
+}
+
 bool walk_fixed(SliceWalk &W, int chunk, SliceOut &o)
 {
     if (!W.init()) return false;
@@ -248,7 +282,7 @@ bool walk_fixed(SliceWalk &W, int chunk, SliceOut &o)
 }  // namespace
 
 int build_long_index(const dtans_container_view *c, int seg_threshold, uint64_t max_words, int chunk,
-                     LongIndex &out)
+                     bool walk, LongIndex &out)
 {
     out = LongIndex();
     const int64_t nsl = c->nslices;
@@ -280,7 +314,11 @@ int build_long_index(const dtans_container_view *c, int seg_threshold, uint64_t 
                 const size_t i = next.fetch_add(1);
                 if (i >= longs.size()) break;
                 int ok = 0;
-                {
+                if (!walk) {
+                    SliceWalk W(c, T, dsym.data(), longs[i]);
+                    plan_fixed(W, chunk, outs[i]);
+                    ok = 1;
+                } else {
                     SliceWalk W(c, T, dsym.data(), longs[i]);
                     ok = walk_fixed(W, chunk, outs[i]) ? 1 : 0;
                     // global-task cursor ends: the next task's start (warp
@@ -304,10 +342,11 @@ int build_long_index(const dtans_container_view *c, int seg_threshold, uint64_t 
     for (auto &x : th) x.join();
     if (bad) return fail(DTANS_E_CORRUPT, "long slice consumed an unexpected number of words");
     // merge in slice order: partial-slot bases and pool offsets
-    std::vector<uint32_t> base(longs.size() + 1, 0);
+    std::vector<uint32_t> base(longs.size() + 1, 0), pbase(longs.size(), 0);
     for (size_t i = 0; i < longs.size(); i++) {
         SliceOut &o = outs[i];
         const uint32_t s = longs[i], pb = base[i], po = (uint32_t)out.pool.size();
+        pbase[i] = po;
         base[i + 1] = pb + o.nparts;
         for (auto tk : o.tasks) {
             tk.slice = s;
@@ -334,7 +373,7 @@ int build_long_index(const dtans_container_view *c, int seg_threshold, uint64_t 
     for (int pass = 0; pass < 2; pass++)
         for (size_t i = 0; i < longs.size(); i++) {
             const uint32_t np = base[i + 1] - base[i];
-            if ((np <= 32) == (pass == 0)) out.slices.push_back(LongSlice{longs[i], base[i], np, 0});
+            if ((np <= 32) == (pass == 0)) out.slices.push_back(LongSlice{longs[i], base[i], np, pbase[i]});
         }
     out.nparts = base.back();
     if (out.pool.empty()) out.pool.push_back(0);

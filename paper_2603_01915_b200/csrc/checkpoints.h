@@ -25,7 +25,7 @@ struct SoloTask {
 };
 
 struct LongSlice {
-    uint32_t slice, part_base, nparts, pad;
+    uint32_t slice, part_base, nparts, pool_base;  // pool_base: the slice's first resume record
 };
 
 struct LongIndex {
@@ -41,7 +41,10 @@ struct LongIndex {
 // buffer), are long: they are split into warp tasks of `chunk` segments, and
 // once a single lane is left at a task boundary its remaining segments
 // become solo tasks of `chunk` segments.
+// walk = false: only the structure (tasks, parts, record offsets and masks);
+// the cursors and resume records are filled by the GPU walk
+// (kernels.cuh dtans_walk_kernel, api.cu).
 int build_long_index(const dtans_container_view *c, int seg_threshold, uint64_t max_words, int chunk,
-                     LongIndex &out);
+                     bool walk, LongIndex &out);
 
 }  // namespace dtans

@@ -612,8 +612,10 @@ __device__ __forceinline__ void full_segment(const KernelArgs &a, const Ctx &C, 
             if (valid) {
                 col += ds[p];
                 if (kDecode) {
-                    a.dec_cols[out_pos] = (int64_t)col;
-                    reinterpret_cast<Bits *>(a.dec_vals)[out_pos] = vs[p];
+                    if (a.dec_cols != nullptr) {  // null: the checkpoint walk only needs the state
+                        a.dec_cols[out_pos] = (int64_t)col;
+                        reinterpret_cast<Bits *>(a.dec_vals)[out_pos] = vs[p];
+                    }
                     out_pos++;
                 } else {
                     xv[p] = __ldg(x + min(col, C.cols_m1));
@@ -736,8 +738,10 @@ __device__ __forceinline__ void final_segment(const KernelArgs &a, const Ctx &C,
         if (base + 2u * p < n) {
             st.col += ds[p];
             if (kDecode) {
-                a.dec_cols[st.out_pos] = (int64_t)st.col;
-                reinterpret_cast<Bits *>(a.dec_vals)[st.out_pos] = vs[p];
+                if (a.dec_cols != nullptr) {
+                    a.dec_cols[st.out_pos] = (int64_t)st.col;
+                    reinterpret_cast<Bits *>(a.dec_vals)[st.out_pos] = vs[p];
+                }
                 st.out_pos++;
             } else {
                 const V xv = __ldg(x + min(st.col, C.cols_m1));
@@ -1340,6 +1344,85 @@ __global__ void __launch_bounds__(256) dtans_solo_kernel(const KernelArgs a)
         }
         if (!ok || cur != tk.cur1 || (tk.j1 == nseg && col > cols_m1)) atomicOr(a.err, !ok || cur != tk.cur1 ? 1u : 2u);
         if (!kDecode) reinterpret_cast<V *>(a.partials)[(size_t)tk.part * 32 + tk.lane] = acc;
+    }
+}
+
+// Checkpoint walk (the GPU pre-pass of the long-slice index): one warp per
+// long slice replays the lockstep decode (decode_range in decode mode with no
+// output arrays) and, at every task boundary j = 0, chunk, 2 chunk, ..., of
+// the host's plan (checkpoints.cpp build_long_index), records the slice
+// cursor in cursors[part] and -- for j > 0 -- the resume record of the
+// lanes still active: {mask, 6 words per lane} for a warp task, the lane's
+// 6 words for a solo task (a single lane left), at the record offsets the
+// host assigned in the same order.  The final cursor must equal the slice's
+// word count.  WalkSrc hooks the per-segment prepare() of decode_range.
+template <typename V> struct WalkSrc {
+    const uint32_t *p;        // &stream[directory[s]]
+    const LaneState<V> *st;   // the walking lanes' state (read at segment starts)
+    uint32_t *pool;           // this slice's first resume record
+    uint32_t *cursors;        // cursors[part_base + k]
+    uint32_t n, chunk, j, k;  // lane's row symbols; segments per task; segment; boundary
+    __device__ __forceinline__ uint32_t operator()(uint32_t rel) const { return __ldg(p + rel); }
+    __device__ __forceinline__ void prepare(uint32_t cur)
+    {
+        if (j % chunk == 0u) {  // uniform
+            const int lane = threadIdx.x & 31;
+            if (lane == 0) cursors[k] = cur;
+            if (j > 0u) {
+                const uint32_t mask = __ballot_sync(0xFFFFFFFFu, ((n + 7u) >> 3) > j);
+                const bool act = (mask >> lane) & 1u;
+                const uint32_t rk = __popc(mask & lanemask_lt());
+                uint32_t *rec = pool;
+                if (__popc(mask) == 1u) {
+                    pool += 6;
+                } else {
+                    if (lane == 0) rec[0] = mask;
+                    rec += 1 + 6 * rk;
+                    pool += 1 + 6 * __popc(mask);
+                }
+                if (act) {
+                    rec[0] = st->w0;
+                    rec[1] = st->w1;
+                    rec[2] = st->w2;
+                    rec[3] = st->d;
+                    rec[4] = st->r;
+                    rec[5] = st->col;
+                }
+            }
+            k++;
+        }
+        j++;
+    }
+};
+
+template <typename V, bool kDIn>
+__global__ void __launch_bounds__(256) dtans_walk_kernel(const KernelArgs a, uint32_t *pool, uint32_t *cursors,
+                                                         uint32_t *final_cur, uint32_t chunk)
+{
+    const bool aligned = load_tables(a);
+    __syncthreads();
+    if (!aligned) {
+        if (threadIdx.x == 0) atomicOr(a.err, 4u);
+        return;
+    }
+    const int lane = threadIdx.x & 31;
+    const Ctx C = make_ctx<V>(a, lane);
+    const uint32_t warps = blockDim.x >> 5;
+    for (uint32_t i = blockIdx.x * warps + (threadIdx.x >> 5); i < a.nlong; i += gridDim.x * warps) {
+        const LongSlice ls = a.longs[i];
+        const uint32_t row = ls.slice * kSliceRows + lane;
+        const uint32_t n = row < (uint32_t)a.rows ? __ldg(a.row_symbols + row) : 0u;
+        uint32_t max_nseg, min_nseg, np;
+        slice_shape(C, n, max_nseg, min_nseg, np);
+        const uint64_t d0 = __ldg(a.directory + ls.slice);
+        const uint32_t nw = (uint32_t)(__ldg(a.directory + ls.slice + 1) - d0);
+        LaneState<V> st;
+        st.out_pos = 0;
+        WalkSrc<V> src{a.stream + d0, &st, pool + ls.pool_base, cursors + ls.part_base, n, chunk, 0u, 0u};
+        init_state<V>(C, src, n, st);
+        const bool ok = decode_range<V, true, kDIn>(a, C, nullptr, src, nw, n, max_nseg, min_nseg, np, 0u, max_nseg,
+                                                    st, lane);
+        if (lane == 0) final_cur[i] = ok ? st.cur : 0xFFFFFFFFu;
     }
 }
 

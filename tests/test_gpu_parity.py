@@ -210,3 +210,29 @@ def test_streamed_upload_from_mmapped_file(gen, tmp_path, monkeypatch):
     assert G.check_spmv(out, ref, m, x, y, c=c)
     assert P.decode_matrix(c) == P.CsrMatrix(m.rows, m.cols, m.row_start, m.col_idx,
                                              m.values.astype(c.value_dtype))
+
+
+@pytest.mark.parametrize("long_seg,chunk", [("4", "3"), ("64", "16"), ("0", "16")])
+def test_gpu_checkpoint_walk_matches_host_walk(long_seg, chunk, monkeypatch):
+    """The long-slice index built by the GPU walk (dtans_walk_kernel, the
+    default) and by the host walk (DTANS_GPU_WALK=0, checkpoints.cpp) give
+    bitwise identical products and decodes, warp and solo tasks included,
+    and both match the oracle within the split-row tolerance."""
+    monkeypatch.setenv("DTANS_LONG_SEG", long_seg)
+    monkeypatch.setenv("DTANS_CHUNK", chunk)
+    for gen in (lambda: synth.rmat(13, 80000, seed=9), lambda: synth.rmat(12, 50000, seed=2, dtype=np.float64),
+                lambda: P.sort_rows_by_length(synth.rmat(13, 90000, seed=4))[0]):
+        m = gen()
+        x, y = synth.vectors(m)
+        outs, decs = [], []
+        for walk in ("1", "0"):
+            monkeypatch.setenv("DTANS_GPU_WALK", walk)
+            c = _fresh(P.encode_matrix(m))
+            assert c.device(0).plan()["nlong"] > 0
+            outs.append(P.spmv(c, x, y))
+            decs.append(P.decode_matrix(c))
+        assert G.same_bits_or_nan(outs[0], outs[1])
+        assert decs[0] == decs[1] == P.CsrMatrix(m.rows, m.cols, m.row_start, m.col_idx,
+                                                 m.values.astype(c.value_dtype))
+        ref = O.spmv(O.parse(P.serialize(c)), x, y, threads=8)
+        assert G.check_spmv(outs[0], ref, m, x, y, c=c)
