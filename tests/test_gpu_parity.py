@@ -212,7 +212,7 @@ def test_streamed_upload_from_mmapped_file(gen, tmp_path, monkeypatch):
                                              m.values.astype(c.value_dtype))
 
 
-@pytest.mark.parametrize("long_seg,chunk", [("4", "3"), ("64", "16"), ("0", "16")])
+@pytest.mark.parametrize("long_seg,chunk", [("4", "3"), ("8", "5"), ("0", "16")])
 def test_gpu_checkpoint_walk_matches_host_walk(long_seg, chunk, monkeypatch):
     """The long-slice index built by the GPU walk (dtans_walk_kernel, the
     default) and by the host walk (DTANS_GPU_WALK=0, checkpoints.cpp) give
