@@ -41,6 +41,7 @@ struct dtans_dev {
     int64_t staged_slices = 0;  // slices whose stream fits a ring buffer
     bool pend = false;          // main kernel instantiation with pending products (kernels.cuh kPend)
     bool host_walk = false;     // long-slice index walked on the host (DTANS_GPU_WALK=0)
+    void *stager = nullptr;     // HostStager: pinned staging of pageable host buffers (dtans_spmv_host)
     std::vector<uint32_t> split_slices;  // slices whose rows sum several task partials
     size_t upload_staged_bytes = 0;  // bytes streamed through the pinned upload buffers
     int64_t upload_batches = 0;
@@ -557,6 +558,84 @@ int gpu_walk(dtans_dev *h, const TableBlock &tb, const SmemPlan &sp, const dtans
     return DTANS_OK;
 }
 
+// Pageable host buffers (the drop-in spmv's numpy arrays): copies go
+// through two pinned staging buffers, filled / drained by worker threads
+// while the other buffer's cudaMemcpyAsync runs -- the driver's own pageable
+// path is several times slower.
+struct HostStager {
+    static constexpr size_t kCap = (size_t)16 << 20;
+    void *buf[2] = {nullptr, nullptr};
+    cudaEvent_t ev[2] = {nullptr, nullptr};
+    bool ready = false;
+    int init()
+    {
+        if (ready) return DTANS_OK;
+        for (int b = 0; b < 2; b++) {
+            CK(cudaHostAlloc(&buf[b], kCap, cudaHostAllocDefault), "cudaHostAlloc staging");
+            CK(cudaEventCreateWithFlags(&ev[b], cudaEventDisableTiming), "event");
+        }
+        ready = true;
+        return DTANS_OK;
+    }
+    static void pcopy(char *dst, const char *src, size_t n)
+    {
+        parallel_for((n + (1u << 20) - 1) >> 20, [&](size_t lo, size_t hi) {
+            memcpy(dst + (lo << 20), src + (lo << 20), std::min(n, hi << 20) - (lo << 20));
+        });
+    }
+    int h2d(void *dst, const void *src, size_t n, cudaStream_t st)
+    {
+        int b = 0;
+        for (size_t o = 0; o < n; o += kCap, b ^= 1) {
+            const size_t len = std::min(kCap, n - o);
+            CK(cudaEventSynchronize(ev[b]), "staging wait");
+            pcopy((char *)buf[b], (const char *)src + o, len);
+            CK(cudaMemcpyAsync((char *)dst + o, buf[b], len, cudaMemcpyHostToDevice, st), "staged H2D");
+            CK(cudaEventRecord(ev[b], st), "event");
+        }
+        return DTANS_OK;
+    }
+    int d2h(void *dst, const void *src, size_t n, cudaStream_t st)
+    {
+        // piece i+1's copy is in flight while piece i is drained
+        const size_t np = (n + kCap - 1) / kCap;
+        for (size_t i = 0; i <= np; i++) {
+            if (i < np) {
+                const size_t o = i * kCap, len = std::min(kCap, n - o);
+                CK(cudaEventSynchronize(ev[i & 1]), "staging wait");
+                CK(cudaMemcpyAsync(buf[i & 1], (const char *)src + o, len, cudaMemcpyDeviceToHost, st), "staged D2H");
+                CK(cudaEventRecord(ev[i & 1], st), "event");
+            }
+            if (i > 0) {
+                const size_t q = i - 1, o = q * kCap, len = std::min(kCap, n - o);
+                CK(cudaEventSynchronize(ev[q & 1]), "staging wait");
+                pcopy((char *)dst + o, (const char *)buf[q & 1], len);
+            }
+        }
+        return DTANS_OK;
+    }
+    ~HostStager()
+    {
+        for (int b = 0; b < 2; b++) {
+            if (ev[b]) cudaEventDestroy(ev[b]);
+            if (buf[b]) cudaFreeHost(buf[b]);
+        }
+    }
+};
+
+void free_stager(void *p) { delete (HostStager *)p; }
+
+bool is_pageable(const void *p)
+{
+    if (!p) return false;
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+        cudaGetLastError();
+        return true;
+    }
+    return at.type == cudaMemoryTypeUnregistered;
+}
+
 // Host->device copies through two pinned staging buffers on one stream:
 // the host fills buffer b while buffer b^1's cudaMemcpyAsync is in flight.
 struct PinnedUploader {
@@ -991,6 +1070,7 @@ extern "C" void dtans_free(dtans_dev *h)
         if (h->ev_in[k]) cudaEventDestroy(h->ev_in[k]);
         if (h->ev_done[k]) cudaEventDestroy(h->ev_done[k]);
     }
+    free_stager(h->stager);
     if (h->st_in) cudaStreamDestroy(h->st_in);
     if (h->st_comp) cudaStreamDestroy(h->st_comp);
     if (h->st_out) cudaStreamDestroy(h->st_out);
@@ -1167,6 +1247,24 @@ extern "C" int dtans_spmv_host(dtans_dev *h, const void *x, const void *y, void 
             CK(cudaEventCreateWithFlags(&h->ev_in[k], cudaEventDisableTiming), "event");
             CK(cudaEventCreateWithFlags(&h->ev_done[k], cudaEventDisableTiming), "event");
         }
+    }
+    if (is_pageable(x) || is_pageable(y) || is_pageable(out)) {
+        // pageable buffers: staged copies in, one launch, staged copies out
+        if (!h->stager) h->stager = new HostStager();
+        HostStager *sg = (HostStager *)h->stager;
+        int rc = sg->init();
+        if (!rc) rc = sg->h2d(dx, x, es * (size_t)h->cols, h->st_comp);
+        if (!rc && y) rc = sg->h2d(dy, y, es * (size_t)h->rows, h->st_comp);
+        if (!rc)
+            rc = h->precision == 8
+                     ? launch<double>(h, (const double *)dx, y ? (const double *)dy : nullptr, (double *)dout, nullptr,
+                                      nullptr, nullptr, false, h->st_comp)
+                     : launch<float>(h, (const float *)dx, y ? (const float *)dy : nullptr, (float *)dout, nullptr,
+                                     nullptr, nullptr, false, h->st_comp);
+        if (!rc) rc = sg->d2h(out, dout, es * (size_t)h->rows, h->st_comp);
+        if (rc) return rc;
+        CK(cudaStreamSynchronize(h->st_comp), "synchronize");
+        return dtans_check(h, h->st_comp);
     }
     const int nch = chunked ? stages : 1;
     CK(cudaMemcpyAsync(dx, x, es * (size_t)h->cols, cudaMemcpyHostToDevice, h->st_in), "H2D x");

@@ -46,6 +46,9 @@
 #ifndef DTANS_LATE_VS
 #define DTANS_LATE_VS 0  // 1: f64 value-dictionary loads after the escape probe (Laplacian +7%: off)
 #endif
+#ifndef DTANS_LAG
+#define DTANS_LAG 0  // 1: lagged accumulation of hot segments (R-MAT +2.8%, spills: off)
+#endif
 #ifndef DTANS_GMEM_CS
 #define DTANS_GMEM_CS 0  // long-slice word loads: 0 L2 evict-first policy, 1 .cs (R-MAT +2.5%), 2 L1::evict_last, 3 __ldg
 #endif
@@ -789,6 +792,33 @@ __device__ __forceinline__ bool decode_range(const KernelArgs &a, const Ctx &C, 
         final_segment<V, kDecode, kDIn, 1, Src, !kDecode>(a, C, x, src, max_nseg - 1, n, st, &pd);
         return true;
     }
+#if DTANS_LAG
+    if (!kDecode && !kPend) {
+        // lagged accumulation (experiment): each hot segment's products are
+        // accumulated after the next segment's gathers are issued
+        Pend4<V> pd;
+        bool have = false;
+        for (; j < jhot; j++) {
+            src.prepare(st.cur);
+            Pend4<V> cur;
+            full_segment<V, kDecode, true, kDIn, Src, true>(a, C, x, src, j, n, nseg, st.w0, st.w1, st.w2, st.d, st.r,
+                                                            st.cur, st.col, st.acc, st.out_pos, lane, &cur);
+            if (have) {
+#pragma unroll
+                for (int p = 0; p < 4; p++)
+                    st.acc = ValueTraits<V>::add(st.acc, ValueTraits<V>::mul(ValueTraits<V>::from_bits(pd.vs[p]), pd.xv[p]));
+            }
+            pd = cur;
+            have = true;
+            if (st.cur > end) return false;  // uniform
+        }
+        if (have) {
+#pragma unroll
+            for (int p = 0; p < 4; p++)
+                st.acc = ValueTraits<V>::add(st.acc, ValueTraits<V>::mul(ValueTraits<V>::from_bits(pd.vs[p]), pd.xv[p]));
+        }
+    }
+#endif
     for (; j < jhot; j++) {
         src.prepare(st.cur);
         full_segment<V, kDecode, true, kDIn>(a, C, x, src, j, n, nseg, st.w0, st.w1, st.w2, st.d, st.r, st.cur,

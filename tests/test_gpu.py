@@ -201,13 +201,19 @@ def test_symmetric_reordered_rmat():
     assert G.same_bits_or_nan(o2.cpu().numpy(), out)
 
 
-def _host_vs_device(c, x, y, stages=None, monkeypatch=None):
+def _host_vs_device(c, x, y, stages=None, monkeypatch=None, pinned=False):
+    """dtans_spmv_host with pageable numpy buffers (staged through the
+    library's pinned buffers) or pinned ones (the pipelined chunk path)."""
     if stages is not None:
         monkeypatch.setenv("DTANS_HOST_STAGES", str(stages))
     dc = c.device(0)
     V = np.float64 if c.precision == 8 else np.float32
-    out = np.full(c.rows, np.nan, dtype=V)
-    dc.spmv_host(np.ascontiguousarray(x, V), None if y is None else np.ascontiguousarray(y, V), out)
+
+    def host(a):
+        a = np.ascontiguousarray(a, V)
+        return torch.from_numpy(a).pin_memory().numpy() if pinned else a
+    out = host(np.full(c.rows, np.nan, dtype=V))
+    dc.spmv_host(host(x), None if y is None else host(y), out)
     xt = torch.from_numpy(np.ascontiguousarray(x, V)).cuda()
     yt = None if y is None else torch.from_numpy(np.ascontiguousarray(y, V)).cuda()
     ref = dc.spmv(xt, yt).cpu().numpy()
@@ -215,19 +221,20 @@ def _host_vs_device(c, x, y, stages=None, monkeypatch=None):
     return out, ref
 
 
+@pytest.mark.parametrize("pinned", [True, False])
 @pytest.mark.parametrize("stages", [1, 8, 32])
 @pytest.mark.parametrize("gen", ["laplacian", "banded", "random"])
-def test_host_buffer_path_matches_device_path(gen, stages, monkeypatch):
-    """dtans_spmv_host (pipelined H2D / kernel on chunk ranges / D2H) equals
-    the device-pointer path bitwise."""
+def test_host_buffer_path_matches_device_path(gen, stages, pinned, monkeypatch):
+    """dtans_spmv_host (pinned: pipelined H2D / kernel on chunk ranges / D2H;
+    pageable: staged copies) equals the device-pointer path bitwise."""
     m = {"laplacian": lambda: synth.laplacian_2d(700),
          "banded": lambda: synth.banded(200000, 27, levels=256, seed=4),
          "random": lambda: synth.config1_random(20000, 300000, seed=3)}[gen]()
     x, y = synth.vectors(m)
     c = P.encode_matrix(m)
-    out, ref = _host_vs_device(c, x, y, stages, monkeypatch)
+    out, ref = _host_vs_device(c, x, y, stages, monkeypatch, pinned)
     assert np.array_equal(out, ref)
-    out0, ref0 = _host_vs_device(c, x, None, stages, monkeypatch)
+    out0, ref0 = _host_vs_device(c, x, None, stages, monkeypatch, pinned)
     assert np.array_equal(out0, ref0)
 
 
