@@ -6,6 +6,8 @@
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
+#include <condition_variable>
+#include <mutex>
 #include <thread>
 #include <vector>
 
@@ -570,6 +572,8 @@ struct HostStager {
     int init()
     {
         if (ready) return DTANS_OK;
+        const unsigned hc = std::thread::hardware_concurrency();
+        pool.start(hc > 1 ? (int)std::min(15u, hc - 1) : 0);
         for (int b = 0; b < 2; b++) {
             CK(cudaHostAlloc(&buf[b], kCap, cudaHostAllocDefault), "cudaHostAlloc staging");
             CK(cudaEventCreateWithFlags(&ev[b], cudaEventDisableTiming), "event");
@@ -577,12 +581,73 @@ struct HostStager {
         ready = true;
         return DTANS_OK;
     }
-    static void pcopy(char *dst, const char *src, size_t n)
-    {
-        parallel_for((n + (1u << 20) - 1) >> 20, [&](size_t lo, size_t hi) {
-            memcpy(dst + (lo << 20), src + (lo << 20), std::min(n, hi << 20) - (lo << 20));
-        });
-    }
+    // memcpy split over a persistent pool of worker threads (the calling
+    // thread takes the first share); pageable destinations also take their
+    // first-touch page faults in parallel
+    struct Pool {
+        std::vector<std::thread> th;
+        std::mutex mu;
+        std::condition_variable cv, done_cv;
+        uint64_t gen = 0;
+        int pending = 0;
+        bool stop = false;
+        char *dst = nullptr;
+        const char *src = nullptr;
+        size_t n = 0;
+        int parts = 1;
+        void run_part(int i)
+        {
+            const size_t lo = n * (size_t)i / (size_t)parts, hi = n * (size_t)(i + 1) / (size_t)parts;
+            if (hi > lo) memcpy(dst + lo, src + lo, hi - lo);
+        }
+        void start(int workers)
+        {
+            parts = workers + 1;
+            for (int w = 0; w < workers; w++)
+                th.emplace_back([this, w]() {
+                    uint64_t seen = 0;
+                    for (;;) {
+                        std::unique_lock<std::mutex> lk(mu);
+                        cv.wait(lk, [&] { return stop || gen != seen; });
+                        if (stop) return;
+                        seen = gen;
+                        lk.unlock();
+                        run_part(w + 1);
+                        lk.lock();
+                        if (--pending == 0) done_cv.notify_one();
+                    }
+                });
+        }
+        void copy(char *d, const char *s, size_t len)
+        {
+            if (th.empty() || len < ((size_t)1 << 20)) {
+                memcpy(d, s, len);
+                return;
+            }
+            {
+                std::lock_guard<std::mutex> lk(mu);
+                dst = d;
+                src = s;
+                n = len;
+                pending = (int)th.size();
+                gen++;
+            }
+            cv.notify_all();
+            run_part(0);
+            std::unique_lock<std::mutex> lk(mu);
+            done_cv.wait(lk, [&] { return pending == 0; });
+        }
+        ~Pool()
+        {
+            {
+                std::lock_guard<std::mutex> lk(mu);
+                stop = true;
+            }
+            cv.notify_all();
+            for (auto &t : th) t.join();
+        }
+    } pool;
+    void pcopy(char *dst, const char *src, size_t n) { pool.copy(dst, src, n); }
     int h2d(void *dst, const void *src, size_t n, cudaStream_t st)
     {
         int b = 0;
