@@ -915,9 +915,13 @@ extern "C" int dtans_upload(const dtans_container_view *c, int device, dtans_dev
         for (int64_t s = 1; s < nsl && sorted; s++)
             sorted = (is_long[s] ? 0 : cost[s]) <= (is_long[s - 1] ? 0 : cost[s - 1]);
         const char *ek = getenv("DTANS_KCHUNK");
+        // slices per chunk: aim at >= 4 chunks per warp, but at least 3 slices
+        // once every warp has work (per-chunk overhead; a strong-scaling shard
+        // of the Laplacian at N=8: -10 %), 1 for matrices smaller than the grid
+        const int64_t grid_warps = (int64_t)sms * h->warps;
         const int64_t kcap = ek ? std::max(1, std::min(atoi(ek), dev::kMaxChunk))
-                                : std::max<int64_t>(1, std::min<int64_t>(dev::kMaxChunk,
-                                                                          nsl / ((int64_t)sms * h->warps * 4)));
+                                : nsl < grid_warps ? 1
+                                : std::max<int64_t>(3, std::min<int64_t>(dev::kMaxChunk, nsl / (grid_warps * 4)));
         uint64_t blob_words = 0;
         bool overflow = false;  // a chunk larger than a staging buffer (planner bug: fail loudly)
         auto push = [&](int64_t s0, int64_t k) {
