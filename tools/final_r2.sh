@@ -9,7 +9,7 @@ run() { local tag=$1; shift; timeout 1200 python bench.py "$@" > gpurun_out/r2f_
 run lap
 run b27 --config banded27 --steps 30
 run rmat_sorted --config rmat --reorder --steps 20 --no-cpu-baseline
-run rmat --config rmat --steps 20 --no-cpu-baseline
+run rmat --config rmat --steps 20
 run powerit --config powerit --steps 20
 run config1 --config config1 --steps 50
 run ref --impl reference --steps 3 --warmup 1
