@@ -49,6 +49,9 @@
 #ifndef DTANS_LAG
 #define DTANS_LAG 0  // 1: lagged accumulation of hot segments (R-MAT +2.8%, spills: off)
 #endif
+#ifndef DTANS_MEDIUM
+#define DTANS_MEDIUM 1  // the medium payload path (every lane <= two one-word payloads)
+#endif
 #ifndef DTANS_GMEM_CS
 #define DTANS_GMEM_CS 0  // long-slice word loads: 0 L2 evict-first policy, 1 .cs (R-MAT +2.5%), 2 L1::evict_last, 3 __ldg
 #endif
@@ -393,7 +396,7 @@ __device__ __forceinline__ void lookup_pair(const Ctx &C, uint32_t sod, uint32_t
 //   payload_probe: 0 = no escape in the warp, 1 = fast case (every lane needs
 //   at most one payload word: its rank among the escaping lanes; f64 value
 //   escapes never qualify), 2 = general case.
-template <typename T, int NP = 4>
+template <typename T, int NP = 4, bool kMedium = false>
 __device__ __forceinline__ int payload_probe(const Ctx &C, const bool act, const uint32_t e[8], bool &dany)
 {
     const uint32_t FULL = 0xFFFFFFFFu;
@@ -440,7 +443,54 @@ __device__ __forceinline__ int payload_probe(const Ctx &C, const bool act, const
         }
         fast = !act || nd + nv <= 1;
     }
-    return __all_sync(FULL, fast) ? 1 : 2;
+    if (__all_sync(FULL, fast)) return 1;
+    if (kMedium && DTANS_MEDIUM) {
+        // 3 = medium case: every lane needs at most two one-word payloads
+        // (deltas, or f32 values)
+        int nd = 0, nv = 0;
+#pragma unroll
+        for (int p = 0; p < NP; p++) {
+            nd += e[2 * p] >= C.desc_min ? 1 : 0;
+            nv += e[2 * p + 1] >= C.vesc_min ? 1 : 0;
+        }
+        const bool med = !act || (T::kPayloadWords == 2 ? (nv == 0 && nd <= 2) : nd + nv <= 2);
+        if (__all_sync(FULL, med)) return 3;
+    }
+    return 2;
+}
+
+// Medium payload event: every lane reads at most two words (one-word
+// payloads), at its offset from a two-plane ballot scan; the escaped slots
+// take them in slot order.  Two loads instead of one per escaped slot.
+template <typename T, class Src>
+__device__ __forceinline__ void payload_medium(const Ctx &C, const Src &src, uint32_t &cur, const bool act,
+                                               const uint32_t e[8], uint32_t ds[4], typename T::Bits vs[4])
+{
+    using Bits = typename T::Bits;
+    const uint32_t FULL = 0xFFFFFFFFu;
+    uint32_t pc = 0;
+#pragma unroll
+    for (int p = 0; p < 4; p++)
+        pc += (e[2 * p] >= C.desc_min ? 1u : 0u) + (T::kPayloadWords == 1 && e[2 * p + 1] >= C.vesc_min ? 1u : 0u);
+    if (!act) pc = 0;
+    const uint32_t b0 = __ballot_sync(FULL, pc & 1u);
+    const uint32_t b1 = __ballot_sync(FULL, pc & 2u);
+    const uint32_t off = cur + __popc(b0 & C.lt) + (__popc(b1 & C.lt) << 1);
+    cur += __popc(b0) + (__popc(b1) << 1);
+    const uint32_t w0 = pc >= 1u ? src(off) : 0u;
+    const uint32_t w1 = pc >= 2u ? src(off + 1u) : 0u;
+    bool second = false;
+#pragma unroll
+    for (int p = 0; p < 4; p++) {
+        if (e[2 * p] >= C.desc_min) {
+            ds[p] = second ? w1 : w0;
+            second = true;
+        }
+        if (T::kPayloadWords == 1 && e[2 * p + 1] >= C.vesc_min) {
+            vs[p] = (Bits)(second ? w1 : w0);
+            second = true;
+        }
+    }
 }
 
 // Fast payload event: every lane reads at most one word, at its rank among
@@ -669,7 +719,7 @@ __device__ __forceinline__ void full_segment(const KernelArgs &a, const Ctx &C, 
         }
     };
     bool dany;
-    const int pk = payload_probe<T>(C, act, e, dany);
+    const int pk = payload_probe<T, 4, true>(C, act, e, dany);
     if (pk == 2) {
         if (kLate) load_vs();
         payload_slow<T>(C, src, cur, act, e, ds, vs);
@@ -677,6 +727,7 @@ __device__ __forceinline__ void full_segment(const KernelArgs &a, const Ctx &C, 
         return;
     }
     if (pk == 1) payload_fast<T>(C, src, cur, act, dany, e, ds, vs);
+    else if (pk == 3) payload_medium<T>(C, src, cur, act, e, ds, vs);
     if (kLate) load_vs();
     rest(ds, vs);
 }
