@@ -50,7 +50,7 @@
 #define DTANS_LAG 0  // 1: lagged accumulation of hot segments (R-MAT +2.8%, spills: off)
 #endif
 #ifndef DTANS_MEDIUM
-#define DTANS_MEDIUM 1  // the medium payload path (every lane <= two one-word payloads)
+#define DTANS_MEDIUM 1  // the medium payload path (f64: every lane <= two escaped deltas)
 #endif
 #ifndef DTANS_GMEM_CS
 #define DTANS_GMEM_CS 0  // long-slice word loads: 0 L2 evict-first policy, 1 .cs (R-MAT +2.5%), 2 L1::evict_last, 3 __ldg
@@ -444,9 +444,10 @@ __device__ __forceinline__ int payload_probe(const Ctx &C, const bool act, const
         fast = !act || nd + nv <= 1;
     }
     if (__all_sync(FULL, fast)) return 1;
-    if (kMedium && DTANS_MEDIUM) {
-        // 3 = medium case: every lane needs at most two one-word payloads
-        // (deltas, or f32 values)
+    if (kMedium && DTANS_MEDIUM && T::kPayloadWords == 2) {
+        // 3 = medium case (f64): every lane needs at most two one-word
+        // payloads (two escaped deltas); banded-27 -0.8 %, while for f32
+        // (R-MAT: many lanes with more escapes) the extra probe cost +1-5 %
         int nd = 0, nv = 0;
 #pragma unroll
         for (int p = 0; p < NP; p++) {
