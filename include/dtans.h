@@ -186,9 +186,12 @@ void dtans_mg_free(dtans_mg *g);
 int dtans_mg_power_iteration(dtans_mg *g, dtans_dev *h, const int64_t *row_off, void *x, int iters,
                              double *lambda_out, void *stream);
 
-/* Same product with HOST x, y, out (pageable or pinned): H2D copy, kernel,
- * D2H copy, synchronize, consumption check.  The end-to-end entry point a
- * ctypes binding of spmv(c, x, y) calls. */
+/* Same product with HOST x, y, out (replaces spmv, container.py:554-596, for
+ * a ctypes binding of spmv(c, x, y)): H2D copy, kernel, D2H copy,
+ * synchronize, consumption check.  Pinned buffers are pipelined over slice
+ * ranges on three streams (H2D / kernel / D2H); pageable buffers (numpy) are
+ * staged through the handle's two pinned buffers by a pool of worker
+ * threads, overlapping the host copies with the DMA. */
 int dtans_spmv_host(dtans_dev *h, const void *x, const void *y, void *out);
 
 /* Bit-exact decode on device: row_start (device, rows+1, int64) must be
