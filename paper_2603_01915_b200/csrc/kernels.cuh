@@ -52,9 +52,6 @@
 #ifndef DTANS_MEDIUM
 #define DTANS_MEDIUM 1  // the medium payload path (f64: every lane <= two escaped deltas)
 #endif
-#ifndef DTANS_SCALED_CS
-#define DTANS_SCALED_CS 0  // 1: the scaled (power-iteration) kernel streams y' past L2 like the others
-#endif
 #ifndef DTANS_GMEM_CS
 #define DTANS_GMEM_CS 0  // long-slice word loads: 0 L2 evict-first policy, 1 .cs (R-MAT +2.5%), 2 L1::evict_last, 3 __ldg
 #endif
@@ -1037,10 +1034,7 @@ __device__ __forceinline__ void decode_slice(const KernelArgs &a, const Ctx &C, 
             res = T::mul(res, scale);
             wsum = __dadd_rn(wsum, __dmul_rn((double)res, (double)res));
         }
-        // power iteration: y' is the next step's x (gathered): keep it in L2
-        // unless DTANS_SCALED_CS
-        if (kScaled && !DTANS_SCALED_CS) reinterpret_cast<V *>(a.out)[orow] = res;
-        else st_stream(reinterpret_cast<V *>(a.out) + orow, res);
+        st_stream(reinterpret_cast<V *>(a.out) + orow, res);
     }
 }
 
