@@ -52,6 +52,9 @@
 #ifndef DTANS_MEDIUM
 #define DTANS_MEDIUM 1  // the medium payload path (f64: every lane <= two escaped deltas)
 #endif
+#ifndef DTANS_PEND2
+#define DTANS_PEND2 1  // the pending-products instantiation's direct path for 2-segment uniform slices
+#endif
 #ifndef DTANS_GMEM_CS
 #define DTANS_GMEM_CS 0  // long-slice word loads: 0 L2 evict-first policy, 1 .cs (R-MAT +2.5%), 2 L1::evict_last, 3 __ldg
 #endif
@@ -1023,8 +1026,21 @@ __device__ __forceinline__ void decode_slice(const KernelArgs &a, const Ctx &C, 
     if (max_nseg != 0u) {  // uniform; an all-empty slice has no words (y' = +0.0 + y)
         if (kDecode && inrow) st.out_pos = __ldg(a.row_start + row);
         init_state<V>(C, src, n, st);
-        ok = decode_range<V, kDecode, kDIn, SmemSrc, kPend>(a, C, x, src, end, n, max_nseg, min_nseg, np, 0u,
-                                                            max_nseg, st, lane);
+#if DTANS_PEND2
+        if (kPend && !kDecode && (meta & 0xFFFF0000u) == ((2u << 16) | (2u << 23))) {
+            // uniform; the pending-products slice shape every 5-point
+            // Laplacian slice has: two segments in every row, a one-pair final
+            // segment (max_nseg = min_nseg = 2, np = 1) -- decode_range's pend
+            // branch without its loop bookkeeping
+            Pend4<V> pd;
+            full_segment<V, kDecode, true, kDIn, SmemSrc, true>(a, C, x, src, 0u, n, 2u, st.w0, st.w1, st.w2, st.d,
+                                                                 st.r, st.cur, st.col, st.acc, st.out_pos, lane, &pd);
+            ok = st.cur <= end;
+            if (ok) final_segment<V, kDecode, kDIn, 1, SmemSrc, true>(a, C, x, src, 1u, n, st, &pd);
+        } else
+#endif
+            ok = decode_range<V, kDecode, kDIn, SmemSrc, kPend>(a, C, x, src, end, n, max_nseg, min_nseg, np, 0u,
+                                                                max_nseg, st, lane);
     }
     bad |= bad_bits(C, ok, st.cur, end, n, st.col);
     if (!kDecode && inrow) {

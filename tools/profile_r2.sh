@@ -68,4 +68,6 @@ for c in $CFGS; do
         --title "Round 2, config 5 (power iteration, banded-32 2^29 nnz, f64): scaled y-less kernel, 1x B200" --cmd "tools/profile_r2.sh pit" ;;
   esac
 done
+# the .ncu-rep files are large (gpurun copies back at most 64 MiB): keep the summaries
+rm -f gpurun_out/r2_*.ncu-rep
 ls -la gpurun_out | grep r2_
