@@ -237,6 +237,8 @@ typedef struct {
     int64_t upload_batches;   /* cudaMemcpyAsync batches of the upload */
     int64_t pend;             /* 1: the main kernel defers the last full segment's products past a
                                  one-pair final segment's gathers (chosen per matrix) */
+    int64_t nempty;           /* all-empty slices written by the empty-slice kernel (plans with
+                                 long slices), outside the main kernel's chunks */
 } dtans_plan_t;
 int dtans_plan(const dtans_dev *h, dtans_plan_t *out);
 

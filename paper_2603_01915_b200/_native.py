@@ -74,7 +74,7 @@ class Plan(ctypes.Structure):
         ("dynamic", ctypes.c_int32), ("dinline", ctypes.c_int32),
         ("bufb", ctypes.c_int32), ("nring", ctypes.c_int32),
         ("upload_bytes", ctypes.c_int64), ("upload_batches", ctypes.c_int64),
-        ("pend", ctypes.c_int64),
+        ("pend", ctypes.c_int64), ("nempty", ctypes.c_int64),
     ]
 
 

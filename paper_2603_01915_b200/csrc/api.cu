@@ -42,6 +42,8 @@ struct dtans_dev {
     int64_t launches = 0;
     int64_t staged_slices = 0;  // slices whose stream fits a ring buffer
     bool pend = false;          // main kernel instantiation with pending products (kernels.cuh kPend)
+    int pdl = 2;                // programmatic dependent launch: 1 main -> task -> solo -> finalize,
+                                // 2 task -> solo -> finalize only, 0 off
     bool host_walk = false;     // long-slice index walked on the host (DTANS_GPU_WALK=0)
     void *stager = nullptr;     // HostStager: pinned staging of pageable host buffers (dtans_spmv_host)
     std::vector<uint32_t> split_slices;  // slices whose rows sum several task partials
@@ -51,6 +53,9 @@ struct dtans_dev {
     void *d_long = nullptr;     // tasks + pool + slices + partials
     size_t long_bytes = 0;
     int task_ctas = 0, task_smem = 0, solo_ctas = 0, solo_smem = 0;
+    uint32_t final_big = 0;     // long slices with > 32 partials (a finalize CTA each)
+    uint32_t *d_empty = nullptr;  // all-empty slices (dtans_empty_kernel)
+    bool solo_first = true;     // DTANS_SOLO_FIRST: solo kernel first, tasks beside it by ticket
     uint32_t *d_row_map = nullptr;  // optional output row map (reordered P*A)
     uint32_t *d_col_map = nullptr;  // optional column map (symmetric P*A*P^T): x'[j] = x[map[j]]
     void *d_xperm = nullptr;        // x' scratch (cols values)
@@ -343,6 +348,13 @@ int configure(dtans_dev *h, const TableBlock &tb, const SmemPlan &sp)
             CK(cudaFuncSetAttribute(ktd, cudaFuncAttributeMaxDynamicSharedMemorySize, h->task_smem), "attr");
             CK(cudaFuncSetAttribute(ks, cudaFuncAttributeMaxDynamicSharedMemorySize, h->solo_smem), "attr");
             CK(cudaFuncSetAttribute(ksd, cudaFuncAttributeMaxDynamicSharedMemorySize, h->solo_smem), "attr");
+            if (const char *ec = getenv("DTANS_TASK_CARVE")) {  // shared-memory carve-out preference (percent)
+                const int pc = atoi(ec);
+                CK(cudaFuncSetAttribute(kt, cudaFuncAttributePreferredSharedMemoryCarveout, pc), "carveout");
+                CK(cudaFuncSetAttribute(ktd, cudaFuncAttributePreferredSharedMemoryCarveout, pc), "carveout");
+                CK(cudaFuncSetAttribute(ks, cudaFuncAttributePreferredSharedMemoryCarveout, pc), "carveout");
+                CK(cudaFuncSetAttribute(ksd, cudaFuncAttributePreferredSharedMemoryCarveout, pc), "carveout");
+            }
             CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kt, dev::kTaskWarps * 32, h->task_smem), "occupancy");
             CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pers, ks, 256, h->solo_smem), "occupancy");
             return DTANS_OK;
@@ -380,6 +392,25 @@ __global__ void __launch_bounds__(256) permute_x_kernel(const V *__restrict__ x,
         xp[j] = __ldg(x + __ldg(map + j));
 }
 
+// A long-slice kernel launched after its predecessor with programmatic
+// dependent launch (kernels.cuh pdl_trigger/pdl_wait): it may start on the
+// SMs the predecessor's finished CTAs free.
+template <typename K>
+void launch_chained(bool pdl, K kernel, int grid, int block, int smem, cudaStream_t st, const dev::KernelArgs &a)
+{
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3((unsigned)block);
+    cfg.dynamicSmemBytes = (size_t)smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, kernel, a);
+}
+
 template <typename V>
 int launch(dtans_dev *h, const V *x, const V *y, V *out, const int64_t *row_start, int64_t *cols,
            void *vals, bool decode_only, cudaStream_t st, int64_t c_lo = -1, int64_t c_hi = -1,
@@ -394,7 +425,11 @@ int launch(dtans_dev *h, const V *x, const V *y, V *out, const int64_t *row_star
     }
     const int64_t nch = (int64_t)a.chunk_hi - (int64_t)a.chunk_lo;
     const int ctas = (int)std::max<int64_t>(1, std::min<int64_t>(h->sms, (nch + h->warps - 1) / h->warps));
-    if (a.dynamic) CK(cudaMemsetAsync(a.work_counter, 0, sizeof(uint32_t), st), "reset work counter");
+    // solo kernel first, the task kernel beside it (PDL) taking tickets
+    const bool solo_first = h->pdl != 0 && h->solo_first && a.nsolo > 0 && a.ntasks > 0 && c_lo < 0;
+    a.task_dyn = solo_first ? 1 : 0;
+    if (a.dynamic || a.task_dyn)
+        CK(cudaMemsetAsync(a.work_counter, 0, 2 * sizeof(uint32_t), st), "reset work counters");
     if (h->d_col_map && !decode_only) {
         if (c_lo <= 0) {  // once per product (the pipelined host path gathers before its first chunk)
             const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)h->sms * 8, (h->cols + 255) / 256));
@@ -429,24 +464,43 @@ int launch(dtans_dev *h, const V *x, const V *y, V *out, const int64_t *row_star
     }
     if (scaled && nch <= 0 && sumsq_zero != nullptr)  // the main kernel zeroes it otherwise
         CK(cudaMemsetAsync(sumsq_zero, 0, sizeof(double), st), "zero sum of squares");
+    if (a.nempty && c_lo < 0 && !decode_only) {
+        const int eb = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)h->sms * 8, ((int64_t)a.nempty + 31) / 32));
+        if (y != nullptr)
+            launch_chained(h->pdl == 1 && nch > 0, dev::dtans_empty_kernel<V, true>, eb, 256, 0, st, a);
+        else
+            launch_chained(h->pdl == 1 && nch > 0, dev::dtans_empty_kernel<V, false>, eb, 256, 0, st, a);
+        h->launches++;
+    }
     if (a.nlong && c_lo < 0) {
+        // the first long kernel overlaps the main kernel's tail only when the
+        // main kernel ran in this call (it triggers its dependents early)
+        const bool pdl = h->pdl != 0;
+        bool chain = (h->pdl == 1 && nch > 0) || (pdl && a.nempty > 0 && !decode_only);
         with_long_kernels<V>(h->dinline, [&](auto kt, auto ktd, auto ks, auto ksd) -> int {
-            if (decode_only) {
-                if (a.ntasks) ktd<<<h->task_ctas, dev::kTaskWarps * 32, h->task_smem, st>>>(a);
-                if (a.nsolo) ksd<<<h->solo_ctas, 256, h->solo_smem, st>>>(a);
-            } else {
-                if (a.ntasks) kt<<<h->task_ctas, dev::kTaskWarps * 32, h->task_smem, st>>>(a);
-                if (a.nsolo) ks<<<h->solo_ctas, 256, h->solo_smem, st>>>(a);
+            if (solo_first) {
+                launch_chained(chain, decode_only ? ksd : ks, h->solo_ctas, 256, h->solo_smem, st, a);
+                launch_chained(true, decode_only ? ktd : kt, h->task_ctas, dev::kTaskWarps * 32, h->task_smem, st, a);
+                chain = true;
+                return 0;
+            }
+            if (a.ntasks) {
+                launch_chained(chain, decode_only ? ktd : kt, h->task_ctas, dev::kTaskWarps * 32, h->task_smem, st, a);
+                chain = pdl;
+            }
+            if (a.nsolo) {
+                launch_chained(chain, decode_only ? ksd : ks, h->solo_ctas, 256, h->solo_smem, st, a);
+                chain = pdl;
             }
             return 0;
         });
         h->launches += (a.ntasks ? 1 : 0) + (a.nsolo ? 1 : 0);
-        if (!decode_only) {
-            const unsigned nb = a.nlong_small_blocks + (a.nlong - a.nlong_small);
+        const int nb = (int)(a.nlong_small_blocks + h->final_big);
+        if (!decode_only && nb > 0) {
             if (y != nullptr)
-                dev::dtans_finalize_kernel<V, true><<<nb, 256, 0, st>>>(a);
+                launch_chained(chain, dev::dtans_finalize_kernel<V, true>, nb, 256, 0, st, a);
             else
-                dev::dtans_finalize_kernel<V, false><<<nb, 256, 0, st>>>(a);
+                launch_chained(chain, dev::dtans_finalize_kernel<V, false>, nb, 256, 0, st, a);
             h->launches += 1;
         }
     }
@@ -887,8 +941,10 @@ extern "C" int dtans_upload(const dtans_container_view *c, int device, dtans_dev
         h->base.ntasks = (uint32_t)li.tasks.size();
         h->base.nsolo = (uint32_t)li.solo.size();
         h->base.nlong = (uint32_t)li.slices.size();
-        uint32_t small = 0;
-        while (small < li.slices.size() && li.slices[small].nparts <= 32) small++;
+        uint32_t small = 0, big = 0;
+        while (small < li.slices.size() && li.slices[small].nparts >= 2 && li.slices[small].nparts <= 32) small++;
+        while (small + big < li.slices.size() && li.slices[small + big].nparts > 32) big++;
+        h->final_big = big;
         h->base.nlong_small = small;
         h->base.nlong_small_blocks = (small + 7) / 8;
         h->base.single_direct = 1;
@@ -900,6 +956,34 @@ extern "C" int dtans_upload(const dtans_container_view *c, int device, dtans_dev
     {
         std::vector<uint8_t> is_long((size_t)nsl, 0);
         for (const LongSlice &ls : li.slices) is_long[ls.slice] = 1;
+        // with long slices (no pipelined host path), all-empty slices go to
+        // dtans_empty_kernel instead of the chunk list (DTANS_EMPTY=0: keep)
+        std::vector<uint32_t> empty;
+        const char *ee = getenv("DTANS_EMPTY");
+        if (!li.slices.empty() && !(ee && atoi(ee) == 0)) {
+            for (int64_t s = 0; s < nsl; s++) {
+                if (is_long[s] || c->directory[s + 1] != c->directory[s]) continue;
+                bool all0 = true;
+                for (int64_t i = s * kSlice; i < std::min<int64_t>((s + 1) * kSlice, c->rows) && all0; i++)
+                    all0 = c->row_symbols[i] == 0;
+                if (all0) {
+                    empty.push_back((uint32_t)s);
+                    is_long[s] = 1;  // not in the chunk list
+                }
+            }
+        }
+        if (!empty.empty()) {
+            cudaError_t e = cudaMalloc(&h->d_empty, sizeof(uint32_t) * empty.size());
+            if (e == cudaSuccess)
+                e = cudaMemcpy(h->d_empty, empty.data(), sizeof(uint32_t) * empty.size(), cudaMemcpyHostToDevice);
+            if (e != cudaSuccess) {
+                if (h->d_empty) cudaFree(h->d_empty);
+                delete h;
+                return fail(DTANS_E_NOMEM, "empty-slice list: %s", cudaGetErrorString(e));
+            }
+            h->base.empty_slices = h->d_empty;
+            h->base.nempty = (uint32_t)empty.size();
+        }
         double mean = 0;
         uint32_t mx = 0;
         for (int64_t s = 0; s < nsl; s++) {
@@ -978,6 +1062,8 @@ extern "C" int dtans_upload(const dtans_container_view *c, int device, dtans_dev
             const uint32_t mseg = (maxn + 7u) / 8u;
             if (pads_ok && mseg >= 2 && minseg == mseg && maxn - 8u * (mseg - 1u) <= 2u) pendable++;
         }
+        if (const char *e = getenv("DTANS_PDL")) h->pdl = atoi(e);
+        if (const char *e = getenv("DTANS_SOLO_FIRST")) h->solo_first = atoi(e) != 0;
         const char *ep = getenv("DTANS_PEND");
         h->pend = ep ? atoi(ep) != 0 : (staged > 0 && 2 * pendable >= staged);
     }
@@ -1131,6 +1217,7 @@ extern "C" void dtans_free(dtans_dev *h)
     cudaSetDevice(h->device);
     if (h->d_base) cudaFree(h->d_base);
     if (h->d_long) cudaFree(h->d_long);
+    if (h->d_empty) cudaFree(h->d_empty);
     if (h->d_row_map) cudaFree(h->d_row_map);
     if (h->d_col_map) cudaFree(h->d_col_map);
     if (h->d_xperm) cudaFree(h->d_xperm);
@@ -1234,6 +1321,7 @@ extern "C" int dtans_plan(const dtans_dev *h, dtans_plan_t *out)
     out->upload_bytes = (int64_t)h->upload_staged_bytes;
     out->upload_batches = h->upload_batches;
     out->pend = h->pend ? 1 : 0;
+    out->nempty = h->base.nempty;
     return DTANS_OK;
 }
 

@@ -368,12 +368,14 @@ int build_long_index(const dtans_container_view *c, int seg_threshold, uint64_t 
                      [](const LongTask &a, const LongTask &b) { return a.j1 - a.j0 > b.j1 - b.j0; });
     std::stable_sort(out.solo.begin(), out.solo.end(),
                      [](const SoloTask &a, const SoloTask &b) { return a.j1 - a.j0 > b.j1 - b.j0; });
-    // finalize order: slices with <= 32 partials first (warp per slice), then
-    // the rest (CTA per slice)
-    for (int pass = 0; pass < 2; pass++)
+    // finalize order: slices with 2..32 partials first (warp per slice), then
+    // those with more (CTA per slice); single-task slices last (the task
+    // kernel writes their rows, finalize never visits them)
+    auto pass_of = [](uint32_t np) { return np <= 1 ? 2 : (np <= 32 ? 0 : 1); };
+    for (int pass = 0; pass < 3; pass++)
         for (size_t i = 0; i < longs.size(); i++) {
             const uint32_t np = base[i + 1] - base[i];
-            if ((np <= 32) == (pass == 0)) out.slices.push_back(LongSlice{longs[i], base[i], np, pbase[i]});
+            if (pass_of(np) == pass) out.slices.push_back(LongSlice{longs[i], base[i], np, pbase[i]});
         }
     out.nparts = base.back();
     if (out.pool.empty()) out.pool.push_back(0);

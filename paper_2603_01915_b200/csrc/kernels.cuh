@@ -148,6 +148,7 @@ struct KernelArgs {
     uint32_t ntasks, nlong, nsolo;
     uint32_t nlong_small, nlong_small_blocks;  // finalize: slices with <= 32 partials come first
     int32_t single_direct;                      // single-task slices write y' in the task kernel
+    int32_t task_dyn;                           // task kernel: atomic tickets after the first round
     const LongTask *tasks;
     const SoloTask *solo;
     const uint32_t *ck_pool;
@@ -165,6 +166,9 @@ struct KernelArgs {
     uint32_t embed_stride;        // static stride (CTAs x warps) the blobs' next records were built for; 0: none
     int32_t work_warps;           // main kernel: warps per CTA that decode (the CTA always has kMaxWarps)
     uint32_t *work_counter;       // zeroed before every dynamic launch
+    // all-empty slices of a long-slice plan (y' = +0.0 + y), outside the chunk list
+    const uint32_t *empty_slices;
+    uint32_t nempty;
 };
 
 __device__ __forceinline__ uint32_t lanemask_lt()
@@ -270,6 +274,16 @@ __device__ __forceinline__ void bulk_g2s_stream(uint32_t dst, const void *src, u
         ::"r"(dst), "l"(src), "r"(bytes), "r"(bar)
         : "memory");
 }
+
+// Programmatic dependent launch (api.cu launch_pdl): the main, task and
+// solo kernels let the next kernel of the chain start on the SMs they free
+// (their tails overlap); the task and solo kernels do not read the main
+// kernel's output, so they only wait for their predecessor at the very end
+// (their completion then implies its completion, which keeps the stream
+// order for everything after the chain); finalize waits up front (it reads
+// the partials).  Both are no-ops in a kernel launched without PDL.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
 __device__ __forceinline__ void fence_mbar_init()
 {
@@ -1117,6 +1131,7 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) dtans_kernel(const KernelAr
     // warps that decode: kMaxWarps, fewer for small matrices (api.cu); the
     // whole CTA still copies the tables in
     const uint32_t kWarps = (uint32_t)a.work_warps;
+    pdl_trigger();
     const bool aligned = load_tables(a);
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
@@ -1253,10 +1268,12 @@ constexpr int kTaskWarps = DTANS_TASK_WARPS;  // task kernel CTA size (warps)
 template <typename V, bool kDecode, bool kDIn>
 __global__ void __launch_bounds__(kTaskWarps * 32, 1024 / (kTaskWarps * 32)) dtans_task_kernel(const KernelArgs a)
 {
+    pdl_trigger();
     const bool aligned = load_tables(a);
     __syncthreads();
     if (!aligned) {
         if (threadIdx.x == 0) atomicOr(a.err, 4u);
+        pdl_wait();
         return;
     }
     const int lane = threadIdx.x & 31;
@@ -1271,7 +1288,14 @@ __global__ void __launch_bounds__(kTaskWarps * 32, 1024 / (kTaskWarps * 32)) dta
     // they are scaled and their squares summed like the main kernel's rows
     const V scale = a.sumsq_in != nullptr ? (V)__ddiv_rn(1.0, __dsqrt_rn(*a.sumsq_in)) : V(1);
     double wsum = 0.0;
-    for (uint32_t t = blockIdx.x * warps + warp; t < a.ntasks; t += gridDim.x * warps) {
+    const uint32_t tstride = gridDim.x * warps;
+    // static tasks t, t + tstride, ...; or (a.task_dyn, when the kernel runs
+    // beside the solo kernel and some CTAs start late) tickets past the
+    // static first round from work_counter[1], zeroed per launch
+    uint32_t t = blockIdx.x * warps + warp;
+    while (t < a.ntasks) {
+        uint32_t tnext = t + tstride;
+        if (a.task_dyn && lane == 0) tnext = tstride + atomicAdd(a.work_counter + 1, 1u);
         const LongTask tk = a.tasks[t];
         const uint32_t row = tk.slice * kSliceRows + lane;
         const bool inrow = row < (uint32_t)a.rows;
@@ -1334,12 +1358,14 @@ __global__ void __launch_bounds__(kTaskWarps * 32, 1024 / (kTaskWarps * 32)) dta
                 reinterpret_cast<V *>(a.partials)[(size_t)tk.part * 32 + lane] = st.acc;
             }
         }
+        t = a.task_dyn ? __shfl_sync(0xFFFFFFFFu, tnext, 0) : tnext;
     }
     if (!kDecode && a.sumsq_out != nullptr) {
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) wsum = __dadd_rn(wsum, __shfl_xor_sync(0xFFFFFFFFu, wsum, o));
         if (lane == 0 && wsum != 0.0) atomicAdd(a.sumsq_out, wsum);
     }
+    pdl_wait();
 }
 
 // Solo tasks: one THREAD decodes segments [j0, j1) of the only row still
@@ -1352,10 +1378,12 @@ __global__ void __launch_bounds__(256) dtans_solo_kernel(const KernelArgs a)
 {
     using T = ValueTraits<V>;
     using Bits = typename T::Bits;
+    pdl_trigger();
     const bool aligned = load_tables(a);
     __syncthreads();
     if (!aligned) {
         if (threadIdx.x == 0) atomicOr(a.err, 4u);
+        pdl_wait();
         return;
     }
     const Ctx C = make_ctx<V>(a, (int)(threadIdx.x & 31));
@@ -1443,6 +1471,7 @@ __global__ void __launch_bounds__(256) dtans_solo_kernel(const KernelArgs a)
         if (!ok || cur != tk.cur1 || (tk.j1 == nseg && col > cols_m1)) atomicOr(a.err, !ok || cur != tk.cur1 ? 1u : 2u);
         if (!kDecode) reinterpret_cast<V *>(a.partials)[(size_t)tk.part * 32 + tk.lane] = acc;
     }
+    pdl_wait();
 }
 
 // Checkpoint walk (the GPU pre-pass of the long-slice index): one warp per
@@ -1524,6 +1553,62 @@ __global__ void __launch_bounds__(256) dtans_walk_kernel(const KernelArgs a, uin
     }
 }
 
+// All-empty slices (every row has no symbols, no stream words) of a plan
+// with long slices: y' = +0.0 + y per row (container.py:534-551 with an
+// empty row), scaled like the main kernel's rows in a power iteration.
+// Taken out of the chunk list because a staged chunk pays its per-slice
+// chain (row map -> y -> y') one slice at a time; here each warp keeps four
+// slices' loads in flight (a rows-sorted R-MAT: 142k empty slices).
+template <typename V, bool kHasY>
+__global__ void __launch_bounds__(256) dtans_empty_kernel(const KernelArgs a)
+{
+    using T = ValueTraits<V>;
+    constexpr int kU = 4;
+    pdl_trigger();
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+    const V scale = a.sumsq_in != nullptr ? (V)__ddiv_rn(1.0, __dsqrt_rn(*a.sumsq_in)) : V(1);
+    const V *y = reinterpret_cast<const V *>(a.y);
+    V *out = reinterpret_cast<V *>(a.out);
+    double wsum = 0.0;
+    for (uint32_t i0 = gw; i0 < a.nempty; i0 += kU * nw) {
+        uint32_t orow[kU];
+        bool in[kU];
+#pragma unroll
+        for (int u = 0; u < kU; u++) {
+            const uint32_t i = i0 + (uint32_t)u * nw;
+            const uint32_t row = i < a.nempty ? __ldg(a.empty_slices + i) * kSliceRows + lane : 0xFFFFFFFFu;
+            in[u] = row < (uint32_t)a.rows;
+            orow[u] = row;
+        }
+#pragma unroll
+        for (int u = 0; u < kU; u++)
+            if (in[u] && a.row_map != nullptr) orow[u] = __ldg(a.row_map + orow[u]);
+        V res[kU];
+#pragma unroll
+        for (int u = 0; u < kU; u++) {
+            res[u] = V(0);
+            if (kHasY && in[u]) res[u] = T::add(V(0), ld_stream(y + orow[u]));
+        }
+#pragma unroll
+        for (int u = 0; u < kU; u++) {
+            if (!in[u]) continue;
+            V r = res[u];
+            if (a.sumsq_out != nullptr) {
+                r = T::mul(r, scale);
+                wsum = __dadd_rn(wsum, __dmul_rn((double)r, (double)r));
+            }
+            st_stream(out + orow[u], r);
+        }
+    }
+    if (a.sumsq_out != nullptr) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) wsum = __dadd_rn(wsum, __shfl_xor_sync(0xFFFFFFFFu, wsum, o));
+        if (lane == 0 && wsum != 0.0) atomicAdd(a.sumsq_out, wsum);
+    }
+    pdl_wait();
+}
+
 // Long-slice rows: y' = (sum of the row's task partials) + y, in a fixed
 // order so the result is deterministic.  Each CTA of 8 warps takes 8 slices
 // (warp = slice, lane = row) when the slices have <= 32 partials; a slice
@@ -1537,6 +1622,7 @@ __global__ void __launch_bounds__(256) dtans_finalize_kernel(const KernelArgs a)
     __shared__ V red[8][32];
     const uint32_t lane = threadIdx.x & 31u, w = threadIdx.x >> 5;
     const V *parts = reinterpret_cast<const V *>(a.partials);
+    pdl_wait();  // the task and solo kernels' partials
     // power iteration (sumsq_out set): scale, and sum the squares (one f64
     // atomic per warp)
     auto finish = [&](const LongSlice &ls, V s) {
