@@ -1144,6 +1144,10 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) dtans_kernel(const KernelAr
         fence_mbar_init();
     }
     __syncthreads();
+    // launched with PDL after the previous product's main kernel (api.cu
+    // pdl_main): the table copy above overlapped its tail; x, y, the output
+    // and the sums of squares are touched only after it has completed
+    pdl_wait();
     if (!aligned) {  // shared-window layout assumption broken: fail loudly
         if (threadIdx.x == 0) atomicOr(a.err, 4u);
         return;
