@@ -39,6 +39,7 @@
 // r = hi32(r'); else load (d', r' already fit 32 bits).
 #pragma once
 #include <cstdint>
+#include <type_traits>
 
 #include "checkpoints.h"
 
@@ -51,6 +52,16 @@
 #endif
 #ifndef DTANS_MEDIUM
 #define DTANS_MEDIUM 1  // the medium payload path (f64: every lane <= two escaped deltas)
+#endif
+#ifndef DTANS_RORDER
+// next-state loads issued before the column prefix and the x gathers:
+// 1 in the task kernel (global-memory words) and in pending-products
+// segments, 2 everywhere, 0 nowhere (R-MAT sorted -1.1 %, natural -1.0 %,
+// Laplacian -0.9 %; banded-27 +0.7 % with 2)
+#define DTANS_RORDER 1
+#endif
+#ifndef DTANS_TICKET_AHEAD
+#define DTANS_TICKET_AHEAD 0  // task kernel: claim the next ticket a task ahead and prefetch its record
 #endif
 #ifndef DTANS_PEND2
 #define DTANS_PEND2 1  // the pending-products instantiation's direct path for 2-segment uniform slices
@@ -676,23 +687,27 @@ __device__ __forceinline__ void full_segment(const KernelArgs &a, const Ctx &C, 
     // the rest of the segment once the symbols are final
     auto rest = [&](const uint32_t (&ds)[4], const Bits (&vs)[4]) __attribute__((always_inline)) {
         V xv[4];
+        auto gathers = [&]() __attribute__((always_inline)) {
 #pragma unroll
-        for (int p = 0; p < 4; p++) {
-            const bool valid = kHot || 8u * j + 2u * p < n;
-            xv[p] = V(0);
-            if (valid) {
-                col += ds[p];
-                if (kDecode) {
-                    if (a.dec_cols != nullptr) {  // null: the checkpoint walk only needs the state
-                        a.dec_cols[out_pos] = (int64_t)col;
-                        reinterpret_cast<Bits *>(a.dec_vals)[out_pos] = vs[p];
+            for (int p = 0; p < 4; p++) {
+                const bool valid = kHot || 8u * j + 2u * p < n;
+                xv[p] = V(0);
+                if (valid) {
+                    col += ds[p];
+                    if (kDecode) {
+                        if (a.dec_cols != nullptr) {  // null: the checkpoint walk only needs the state
+                            a.dec_cols[out_pos] = (int64_t)col;
+                            reinterpret_cast<Bits *>(a.dec_vals)[out_pos] = vs[p];
+                        }
+                        out_pos++;
+                    } else {
+                        xv[p] = __ldg(x + min(col, C.cols_m1));
                     }
-                    out_pos++;
-                } else {
-                    xv[p] = __ldg(x + min(col, C.cols_m1));
                 }
             }
-        }
+        };
+        constexpr bool kRO = DTANS_RORDER == 2 || (DTANS_RORDER == 1 && (kDefer || std::is_same<Src, GmemSrc>::value));
+        if (!kRO) gathers();
         // mixed-radix checks (container.py:478-497): bases decide load vs extract
         uint32_t bm1a, dga, bm1b, dgb;
         group(e[0], e[1], e[2], e[3], bm1a, dga);
@@ -712,6 +727,7 @@ __device__ __forceinline__ void full_segment(const KernelArgs &a, const Ctx &C, 
         const uint32_t lw1 = src(c1 + __popc(m_ld1 & C.lt));
         const uint32_t lw2 = src(c2 + (kHot ? (uint32_t)lane : __popc(m_nl & C.lt)));
         cur = c2 + (kHot ? 32u : __popc(m_nl));
+        if (kRO) gathers();
         if (notlast) {
             uint32_t d1l, d1h, d2l, d2h;
             fold(d, bm1a, dga, d1l, d1h);
@@ -1297,10 +1313,35 @@ __global__ void __launch_bounds__(kTaskWarps * 32, 1024 / (kTaskWarps * 32)) dta
     // beside the solo kernel and some CTAs start late) tickets past the
     // static first round from work_counter[1], zeroed per launch
     uint32_t t = blockIdx.x * warps + warp;
+#if DTANS_TICKET_AHEAD
+    // one ticket ahead: the next task is known a whole task early, so its
+    // record is prefetched into L1 and the ticket's atomic latency is hidden
+    // (inline PTX: the compiler's warp-aggregated atomicAdd waits for the
+    // result right away)
+    uint32_t tn = t + tstride;
+    if (a.task_dyn) {
+        uint32_t v = 0;
+        if (lane == 0) asm volatile("atom.global.add.u32 %0, [%1], 1;" : "=r"(v) : "l"(a.work_counter + 1) : "memory");
+        tn = tstride + __shfl_sync(0xFFFFFFFFu, v, 0);
+    }
+    while (t < a.ntasks) {
+        uint32_t claim = 0;
+        if (a.task_dyn && lane == 0)
+            asm volatile("atom.global.add.u32 %0, [%1], 1;" : "=r"(claim) : "l"(a.work_counter + 1) : "memory");
+        if (lane == 0 && tn < a.ntasks) asm volatile("prefetch.global.L1 [%0];" ::"l"(a.tasks + tn));
+        LongTask tk;
+        {
+            const uint4 *q = reinterpret_cast<const uint4 *>(a.tasks + t);
+            const uint4 u0 = __ldg(q), u1 = __ldg(q + 1);
+            tk.slice = u0.x; tk.j0 = u0.y; tk.j1 = u0.z; tk.part = u0.w;
+            tk.cur0 = u1.x; tk.cur1 = u1.y; tk.ck = u1.z; tk.last = u1.w;
+        }
+#else
     while (t < a.ntasks) {
         uint32_t tnext = t + tstride;
         if (a.task_dyn && lane == 0) tnext = tstride + atomicAdd(a.work_counter + 1, 1u);
         const LongTask tk = a.tasks[t];
+#endif
         const uint32_t row = tk.slice * kSliceRows + lane;
         const bool inrow = row < (uint32_t)a.rows;
         const uint32_t n = inrow ? __ldg(a.row_symbols + row) : 0u;
@@ -1362,7 +1403,13 @@ __global__ void __launch_bounds__(kTaskWarps * 32, 1024 / (kTaskWarps * 32)) dta
                 reinterpret_cast<V *>(a.partials)[(size_t)tk.part * 32 + lane] = st.acc;
             }
         }
+#if DTANS_TICKET_AHEAD
+        const uint32_t tnn = a.task_dyn ? tstride + __shfl_sync(0xFFFFFFFFu, claim, 0) : tn + tstride;
+        t = tn;
+        tn = tnn;
+#else
         t = a.task_dyn ? __shfl_sync(0xFFFFFFFFu, tnext, 0) : tnext;
+#endif
     }
     if (!kDecode && a.sumsq_out != nullptr) {
 #pragma unroll
