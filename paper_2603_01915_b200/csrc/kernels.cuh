@@ -60,9 +60,6 @@
 // Laplacian -0.9 %; banded-27 +0.7 % with 2)
 #define DTANS_RORDER 1
 #endif
-#ifndef DTANS_TICKET_AHEAD
-#define DTANS_TICKET_AHEAD 0  // task kernel: claim the next ticket a task ahead and prefetch its record
-#endif
 #ifndef DTANS_PEND2
 #define DTANS_PEND2 1  // the pending-products instantiation's direct path for 2-segment uniform slices
 #endif
@@ -1313,35 +1310,10 @@ __global__ void __launch_bounds__(kTaskWarps * 32, 1024 / (kTaskWarps * 32)) dta
     // beside the solo kernel and some CTAs start late) tickets past the
     // static first round from work_counter[1], zeroed per launch
     uint32_t t = blockIdx.x * warps + warp;
-#if DTANS_TICKET_AHEAD
-    // one ticket ahead: the next task is known a whole task early, so its
-    // record is prefetched into L1 and the ticket's atomic latency is hidden
-    // (inline PTX: the compiler's warp-aggregated atomicAdd waits for the
-    // result right away)
-    uint32_t tn = t + tstride;
-    if (a.task_dyn) {
-        uint32_t v = 0;
-        if (lane == 0) asm volatile("atom.global.add.u32 %0, [%1], 1;" : "=r"(v) : "l"(a.work_counter + 1) : "memory");
-        tn = tstride + __shfl_sync(0xFFFFFFFFu, v, 0);
-    }
-    while (t < a.ntasks) {
-        uint32_t claim = 0;
-        if (a.task_dyn && lane == 0)
-            asm volatile("atom.global.add.u32 %0, [%1], 1;" : "=r"(claim) : "l"(a.work_counter + 1) : "memory");
-        if (lane == 0 && tn < a.ntasks) asm volatile("prefetch.global.L1 [%0];" ::"l"(a.tasks + tn));
-        LongTask tk;
-        {
-            const uint4 *q = reinterpret_cast<const uint4 *>(a.tasks + t);
-            const uint4 u0 = __ldg(q), u1 = __ldg(q + 1);
-            tk.slice = u0.x; tk.j0 = u0.y; tk.j1 = u0.z; tk.part = u0.w;
-            tk.cur0 = u1.x; tk.cur1 = u1.y; tk.ck = u1.z; tk.last = u1.w;
-        }
-#else
     while (t < a.ntasks) {
         uint32_t tnext = t + tstride;
         if (a.task_dyn && lane == 0) tnext = tstride + atomicAdd(a.work_counter + 1, 1u);
         const LongTask tk = a.tasks[t];
-#endif
         const uint32_t row = tk.slice * kSliceRows + lane;
         const bool inrow = row < (uint32_t)a.rows;
         const uint32_t n = inrow ? __ldg(a.row_symbols + row) : 0u;
@@ -1403,13 +1375,7 @@ __global__ void __launch_bounds__(kTaskWarps * 32, 1024 / (kTaskWarps * 32)) dta
                 reinterpret_cast<V *>(a.partials)[(size_t)tk.part * 32 + lane] = st.acc;
             }
         }
-#if DTANS_TICKET_AHEAD
-        const uint32_t tnn = a.task_dyn ? tstride + __shfl_sync(0xFFFFFFFFu, claim, 0) : tn + tstride;
-        t = tn;
-        tn = tnn;
-#else
         t = a.task_dyn ? __shfl_sync(0xFFFFFFFFu, tnext, 0) : tnext;
-#endif
     }
     if (!kDecode && a.sumsq_out != nullptr) {
 #pragma unroll
