@@ -98,3 +98,60 @@ def test_empty_slices_fused_power_iteration(dtype, monkeypatch):
     xf, xu = xf.cpu().numpy(), xu.cpu().numpy()
     assert np.allclose(xf, xu, rtol=100 * tol, atol=100 * tol / np.sqrt(m.cols))
     assert np.all(xf[1024:1024 + 640] == 0) and not np.signbit(xf[1024:1024 + 640]).any()
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+def test_launch_chain_variants_identical(dtype, monkeypatch):
+    """The long-slice launch chain (api.cu launch: PDL between the solo,
+    task and finalize kernels, solo first with task tickets, the empty-slice
+    kernel, 48-segment tasks for sorted rows) changes only the schedule:
+    every variant gives the same bits, the decode stays bit-exact, and the
+    result matches the oracle under the parity policy."""
+    m, pm, perm, c = _sorted_rmat(dtype)
+    p64 = perm.astype(np.int64)
+    x, y = synth.vectors(m)
+    outs = {}
+    for env in ({}, {"DTANS_PDL": "0"}, {"DTANS_SOLO_FIRST": "0"}, {"DTANS_EMPTY": "0"},
+                {"DTANS_PDL": "1"}, {"DTANS_PDL_MAIN": "0"}):
+        for k in ("DTANS_PDL", "DTANS_SOLO_FIRST", "DTANS_EMPTY", "DTANS_PDL_MAIN"):
+            monkeypatch.delenv(k, raising=False)
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        _fresh(c)
+        outs[tuple(env.items())] = P.spmv(c, x, y)
+        plan = c.device(0).plan()
+        assert plan["nlong"] > 0 and plan["ntasks"] > 0
+        assert (plan["nempty"] > 0) == (env.get("DTANS_EMPTY") != "0")
+        assert P.decode_matrix(c) == pm
+    base = outs[()]
+    for k, o in outs.items():
+        assert G.same_bits_or_nan(o, base), k
+    ref_p = O.spmv(O.parse(P.serialize(c)), x, y[p64], threads=8)
+    assert G.check_spmv(base[p64], ref_p, pm, x, y[p64], c=c)
+
+
+def test_back_to_back_products_on_one_stream():
+    """Consecutive products on one stream overlap through PDL (the main
+    kernel's table copy runs in the previous product's tail): a chain of
+    dependent products (y_{k+1} = A x + y_k) must equal the same chain run
+    with a synchronize between products."""
+    m = synth.laplacian_2d(300)
+    c = P.encode_matrix(m)
+    x, y = synth.vectors(m)
+    dev = c.device(0)
+    xt = torch.from_numpy(x).cuda()
+    ys = [torch.from_numpy(y).cuda()]
+    for _ in range(6):
+        ys.append(dev.spmv(xt, ys[-1]))
+    got = ys[-1].cpu().numpy()
+    yy = torch.from_numpy(y).cuda()
+    for _ in range(6):
+        yy = dev.spmv(xt, yy)
+        torch.cuda.synchronize()
+    dev.check()
+    assert G.same_bits_or_nan(got, yy.cpu().numpy())
+    ref = y.copy()
+    oc = O.parse(P.serialize(c))
+    for _ in range(6):
+        ref = O.spmv(oc, x, ref, threads=8)
+    assert G.same_bits_or_nan(got, ref)
