@@ -1,7 +1,8 @@
 """Small SpMV/decode cases for compute-sanitizer (memcheck / racecheck /
 synccheck): the main kernel (chunks of several slices), the long-slice task
 kernel (streamed windows), the solo and finalize kernels, the scaled power-
-iteration step, and the host-buffer path.  Each result is checked against
+iteration step, the host-buffer path, and a rows-sorted R-MAT through the
+default long-slice launch chain (empty-slice kernel, PDL).  Each result is checked against
 the oracle so a sanitizer run is also a parity run."""
 import os
 import sys
@@ -37,5 +38,30 @@ for name, m in cases:
     oh = np.empty_like(y)
     dev.spmv_host(x, y, oh)
     print(name, "ok", dev.plan())
+# rows-sorted R-MAT with the default planner: every non-empty slice is a
+# task, all-empty slices go to the empty-slice kernel, and the solo, task and
+# finalize launches are chained with programmatic dependent launch; several
+# products back to back on one stream (PDL main kernel)
+os.environ.pop("DTANS_LONG_SEG")
+os.environ.pop("DTANS_KCHUNK")
+m = synth.rmat(13, 60000, seed=5)
+pm, perm = P.sort_rows_by_length(m)
+c = P.encode_matrix(pm)
+c.row_map = perm
+p64 = perm.astype(np.int64)
+x, y = synth.vectors(m)
+out = P.spmv(c, x, y)
+ref = O.spmv(O.parse(P.serialize(c)), x, y[p64], threads=4)
+s = np.abs(pm.values.astype(np.float64)) * np.abs(x.astype(np.float64))[pm.col_idx]
+s = np.bincount(np.repeat(np.arange(pm.rows), np.diff(pm.row_start)), weights=s, minlength=pm.rows) + np.abs(y[p64])
+assert np.all(np.abs(out[p64].astype(np.float64) - ref) <= 1e-5 * s), "rmat sorted"
+dev = c.device(0)
+plan = dev.plan()
+assert plan["nlong"] > 0 and plan["nempty"] > 0, plan
+xt, yt = torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda()
+for _ in range(3):
+    yt = dev.spmv(xt, yt)
+dev.check()
+print("rmat_sorted ok", plan)
 torch.cuda.synchronize()
 print("sanitize cases ok")
