@@ -46,6 +46,7 @@ struct dtans_dev {
                                 // 2 task -> solo -> finalize only, 0 off
     bool host_walk = false;     // long-slice index walked on the host (DTANS_GPU_WALK=0)
     void *stager = nullptr;     // HostStager: pinned staging of pageable host buffers (dtans_spmv_host)
+    unsigned int *h_err = nullptr;  // pinned copy of the error word (host-buffer path)
     std::vector<uint32_t> split_slices;  // slices whose rows sum several task partials
     size_t upload_staged_bytes = 0;  // bytes streamed through the pinned upload buffers
     int64_t upload_batches = 0;
@@ -1234,6 +1235,7 @@ extern "C" void dtans_free(dtans_dev *h)
     if (h->d_col_map) cudaFree(h->d_col_map);
     if (h->d_xperm) cudaFree(h->d_xperm);
     if (h->d_io) cudaFree(h->d_io);
+    if (h->h_err) cudaFreeHost(h->h_err);
     for (int k = 0; k < kHostChunks; k++) {
         if (h->ev_in[k]) cudaEventDestroy(h->ev_in[k]);
         if (h->ev_done[k]) cudaEventDestroy(h->ev_done[k]);
@@ -1438,8 +1440,16 @@ extern "C" int dtans_spmv_host(dtans_dev *h, const void *x, const void *y, void 
     const int nch = chunked ? stages : 1;
     CK(cudaMemcpyAsync(dx, x, es * (size_t)h->cols, cudaMemcpyHostToDevice, h->st_in), "H2D x");
     for (int k = 0; k < nch; k++) {
-        // chunks [c0, c1) cover rows [r0, r1) (natural order when chunked)
-        const int64_t c0 = nchunks * k / nch, c1 = nchunks * (k + 1) / nch;
+        // chunks [c0, c1) cover rows [r0, r1) (natural order when chunked);
+        // the last two stages are short (3/32 and 1/32 of the chunks), so the
+        // tail after the final H2D -- the last kernel and D2H -- is short
+        auto bound = [&](int q) -> int64_t {
+            if (nch < 4) return nchunks * q / nch;
+            if (q >= nch) return nchunks;
+            if (q == nch - 1) return nchunks - nchunks / 32;
+            return (nchunks - nchunks / 8) * q / (nch - 2);  // q <= nch - 2
+        };
+        const int64_t c0 = bound(k), c1 = bound(k + 1);
         int64_t r0 = 0, r1 = h->rows;
         if (chunked) {
             r0 = (int64_t)h->chunks[c0].s0 * kSlice;
@@ -1466,8 +1476,13 @@ extern "C" int dtans_spmv_host(dtans_dev *h, const void *x, const void *y, void 
             CK(cudaMemcpyAsync((char *)out + es * r0, dout + es * r0, es * (size_t)(r1 - r0),
                                cudaMemcpyDeviceToHost, h->st_out), "D2H out");
     }
+    // the error word rides the copy-out stream behind the last chunk (whose
+    // kernel is the last on st_comp): one synchronize for the whole call
+    if (!h->h_err) CK(cudaMallocHost(&h->h_err, sizeof(unsigned int)), "cudaMallocHost error word");
+    CK(cudaMemcpyAsync(h->h_err, h->d_err, sizeof(unsigned int), cudaMemcpyDeviceToHost, h->st_out), "D2H error word");
     CK(cudaStreamSynchronize(h->st_out), "synchronize");
-    return dtans_check(h, h->st_comp);
+    if (*h->h_err) return dtans_check(h, h->st_comp);  // clears it and maps it to the error
+    return DTANS_OK;
 }
 
 extern "C" int dtans_decode(dtans_dev *h, const int64_t *row_start, int64_t *cols, void *valbits,
