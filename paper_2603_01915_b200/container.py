@@ -425,12 +425,22 @@ def spmv(c: CsrDtansContainer, x: np.ndarray, y: np.ndarray, threads: int = 1,
     dtype = c.value_dtype
     x = np.ascontiguousarray(x.astype(dtype, copy=False))
     y = np.ascontiguousarray(y.astype(dtype, copy=False))
-    out = np.empty(c.rows, dtype=dtype)
     if c.rows == 0:
-        return out
+        return np.empty(0, dtype=dtype)
     if c.cols == 0:
         x = np.zeros(1, dtype=dtype)
-    return c.device(device).spmv_host(x, y, out)
+    dev = c.device(device)
+    return dev.spmv_host(x, y, _pinned_empty(c.rows, dtype))
+
+
+def _pinned_empty(n: int, dtype) -> np.ndarray:
+    """A new array in page-locked memory from torch's caching host
+    allocator: the D2H lands in it directly, and an array the caller has
+    dropped is reused (already faulted in) by the next call, instead of a
+    fresh np.empty whose first touch costs page faults (DESIGN 5)."""
+    torch = _torch()
+    tdt = torch.float64 if np.dtype(dtype) == np.float64 else torch.float32
+    return torch.empty(n, dtype=tdt, pin_memory=True).numpy()
 
 
 # ---------------------------------------------------------------------------

@@ -1423,16 +1423,30 @@ extern "C" int dtans_spmv_host(dtans_dev *h, const void *x, const void *y, void 
         // pageable buffers: staged copies in, one launch, staged copies out
         if (!h->stager) h->stager = new HostStager();
         HostStager *sg = (HostStager *)h->stager;
+        // each buffer on its own: pinned ones are copied directly, pageable
+        // ones through the staging buffers
         int rc = sg->init();
-        if (!rc) rc = sg->h2d(dx, x, es * (size_t)h->cols, h->st_comp);
-        if (!rc && y) rc = sg->h2d(dy, y, es * (size_t)h->rows, h->st_comp);
+        auto h2d = [&](void *d, const void *hsrc, size_t n) -> int {
+            if (!is_pageable(hsrc)) {
+                CK(cudaMemcpyAsync(d, hsrc, n, cudaMemcpyHostToDevice, h->st_comp), "H2D");
+                return DTANS_OK;
+            }
+            return sg->h2d(d, hsrc, n, h->st_comp);
+        };
+        if (!rc) rc = h2d(dx, x, es * (size_t)h->cols);
+        if (!rc && y) rc = h2d(dy, y, es * (size_t)h->rows);
         if (!rc)
             rc = h->precision == 8
                      ? launch<double>(h, (const double *)dx, y ? (const double *)dy : nullptr, (double *)dout, nullptr,
                                       nullptr, nullptr, false, h->st_comp)
                      : launch<float>(h, (const float *)dx, y ? (const float *)dy : nullptr, (float *)dout, nullptr,
                                      nullptr, nullptr, false, h->st_comp);
-        if (!rc) rc = sg->d2h(out, dout, es * (size_t)h->rows, h->st_comp);
+        if (!rc) {
+            if (is_pageable(out))
+                rc = sg->d2h(out, dout, es * (size_t)h->rows, h->st_comp);
+            else
+                CK(cudaMemcpyAsync(out, dout, es * (size_t)h->rows, cudaMemcpyDeviceToHost, h->st_comp), "D2H");
+        }
         if (rc) return rc;
         CK(cudaStreamSynchronize(h->st_comp), "synchronize");
         return dtans_check(h, h->st_comp);
