@@ -155,3 +155,27 @@ def test_back_to_back_products_on_one_stream():
     for _ in range(6):
         ref = O.spmv(oc, x, ref, threads=8)
     assert G.same_bits_or_nan(got, ref)
+
+
+def test_device_path_rejects_bad_vectors():
+    """DeviceContainer.spmv validates x, y and out (dtype, length, device,
+    contiguity) before any launch: a short `out` would otherwise be written
+    past its end (round-1 advice)."""
+    m = synth.laplacian_2d(40)
+    c = P.encode_matrix(m)
+    dev = c.device(0)
+    x = torch.zeros(m.cols, dtype=torch.float64, device="cuda")
+    y = torch.zeros(m.rows, dtype=torch.float64, device="cuda")
+    bad = [
+        dict(x=x, y=y, out=torch.empty(m.rows - 1, dtype=torch.float64, device="cuda")),
+        dict(x=x, y=y, out=torch.empty(m.rows, dtype=torch.float32, device="cuda")),
+        dict(x=x, y=y, out=torch.empty(m.rows, dtype=torch.float64)),
+        dict(x=torch.zeros(2 * m.cols, dtype=torch.float64, device="cuda")[::2], y=y, out=None),
+        dict(x=x, y=torch.zeros(m.rows + 1, dtype=torch.float64, device="cuda"), out=None),
+    ]
+    for kw in bad:
+        with pytest.raises(P.ParameterError):
+            dev.spmv(kw["x"], kw["y"], kw["out"])
+    o = dev.spmv(x, y)
+    dev.check()
+    assert o.shape == (m.rows,)
