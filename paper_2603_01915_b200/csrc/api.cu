@@ -879,7 +879,10 @@ extern "C" int dtans_upload(const dtans_container_view *c, int device, dtans_dev
     const char *e1 = getenv("DTANS_LONG_SEG"), *e2 = getenv("DTANS_CHUNK");
     // chunked slices have max_nseg <= long_seg <= kMetaMaxNseg (slice_meta field)
     const int long_seg = std::min<int>(e1 ? atoi(e1) : 64, (int)dev::kMetaMaxNseg);
-    int chunk = e2 ? atoi(e2) : 16;  // rows-sorted plans default to 32 below
+    // 24 segments per task (natural-order R-MAT: 8/12/16/20/24/28/32 gave
+    // 1.622/1.592/1.626/1.663/1.577/1.618/1.648 ms -- non-monotonic, the
+    // task/solo split shifts with it); rows-sorted plans use 48 (below)
+    int chunk = e2 ? atoi(e2) : 24;
     const bool pads_ok = tb.nd > 0 && tb.nv > 0;
     std::vector<uint32_t> cost((size_t)nsl);
     for (int64_t s = 0; s < nsl; s++) {
